@@ -1,0 +1,190 @@
+/*
+ * hd.h -- C ABI of libhd.so, the B200 (sm_100a) hot path of the hitdns
+ * compressible Navier-Stokes solver: WENO5 + Roe hyperbolic sweeps,
+ * 4th-order central viscous terms, RK4/RK3 stage updates, CFL and
+ * diagnostic reductions.
+ *
+ * Conventions (identical to the reference FieldSet, pkg/src/hitdns/grid.py:1-21):
+ *   - a state is one flat fp64 buffer of 5 * total_points doubles, layout
+ *     COMPONENT_CONTIGUOUS (var * total_points + point), x fastest, with
+ *     `ghost` ghost layers on each side of each axis;
+ *   - variables are [rho, rho*u, rho*v, rho*w, E].
+ * All pointers are DEVICE pointers owned by the caller (torch); no call
+ * allocates device memory except hd_plan_create (host-side plan struct).
+ * Every compute call is asynchronous on the given cudaStream_t (passed as
+ * void*, 0 = legacy default stream) and returns 0 or a negative HD_E* code.
+ * Invalid states (rho <= 0 or p <= 0, physics.py:47-55) are not returned by
+ * the call: they are latched in a device error key read by hd_error_read().
+ */
+#ifndef HD_H_
+#define HD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HD_ABI_VERSION 1
+
+/* status codes */
+#define HD_OK 0
+#define HD_E_ARG -1      /* bad argument / geometry */
+#define HD_E_CUDA -2     /* a CUDA launch or API call failed */
+#define HD_E_WORKSPACE -3 /* workspace missing or too small */
+#define HD_E_UNSUPPORTED -4
+
+/* arithmetic modes */
+#define HD_MODE_FAST 0  /* FMA, one reciprocal per WENO reconstruction, shared betas */
+#define HD_MODE_EXACT 1 /* reference operation order, no contraction: bitwise equal to the reference */
+
+/* steppers (timeint.py:196 STEPPERS) */
+#define HD_SCHEME_RK3 3
+#define HD_SCHEME_RK4 4
+
+/* stage parts for decomposed runs (hd_stage_part) */
+#define HD_PART_LOCAL 1   /* sweeps along locally-periodic axes */
+#define HD_PART_HALO 2    /* sweeps along exchanged axes + viscous fluxes */
+#define HD_PART_DIVLOC 4  /* viscous divergence along locally-periodic axes */
+#define HD_PART_UPDATE 8  /* divergence along exchanged axes + RK stage update */
+#define HD_PART_ALL 15
+
+/* workspace buffers (hd_plan_buffer) */
+#define HD_BUF_STAGE 0 /* 5 fields: RK stage state */
+#define HD_BUF_ACC 1   /* 5 fields: RK4 accumulator */
+#define HD_BUF_INC 2   /* 5 fields: RHS increment */
+#define HD_BUF_PRIM 3  /* 4 fields: u, v, w, T */
+#define HD_BUF_VFLUX 4 /* 12 fields: viscous flux F_d[r], d-major */
+#define HD_BUF_RED 5   /* reduction partials + results */
+#define HD_BUF_CTX 6   /* step context: t, dt, ... */
+#define HD_BUF_ERR 7   /* error key (uint64) */
+#define HD_NBUF 8
+
+/* results of hd_reduce_state (doubles at HD_BUF_RED result slot) */
+#define HD_RED_SIGNAL_MAX 0
+#define HD_RED_SIGNAL_SUM 1
+#define HD_RED_WAVESPEED 2
+#define HD_RED_MASS 3     /* plain sums; multiply by cell volume */
+#define HD_RED_MOMX 4
+#define HD_RED_MOMY 5
+#define HD_RED_MOMZ 6
+#define HD_RED_ENERGY 7
+#define HD_RED_KE 8       /* sum of 0.5*|m/rho|^2 */
+#define HD_RED_N 9
+
+/* context slots (doubles at HD_BUF_CTX) */
+#define HD_CTX_T 0
+#define HD_CTX_DT 1
+#define HD_CTX_N 4
+
+typedef struct hd_geom {
+  int n[3];            /* interior cells per axis (x, y, z) of THIS rank's block */
+  double length[3];    /* box length per axis of this block (spacing = length/n) */
+  int ghost;           /* ghost width g >= 3 (grid.py:69-70) */
+  int periodic[3];     /* 1: axis wraps locally; 0: ghosts come from a halo exchange */
+} hd_geom;
+
+typedef struct hd_gas {     /* physics.py:26-44 GasModel */
+  double gamma, prandtl, mu, visc_scale;
+} hd_gas;
+
+typedef struct hd_weno {    /* weno.py:40-55 WenoParams + entropy-fix delta (kernels.py:60) */
+  double epsilon;
+  int power;
+  double delta;
+} hd_weno;
+
+typedef struct hd_plan hd_plan;
+
+int hd_abi_version(void);
+const char* hd_status_string(int status);
+
+/* Workspace bytes a plan needs (stage/acc/inc/prims/viscous fluxes/reductions). */
+int64_t hd_workspace_bytes(const hd_geom* geom);
+
+/* Create a plan on the current device.  `workspace` (device, >= hd_workspace_bytes,
+ * 256-byte aligned) stays owned by the caller and must outlive the plan. */
+int hd_plan_create(const hd_geom* geom, const hd_gas* gas, const hd_weno* weno, int mode,
+                   void* workspace, int64_t workspace_bytes, hd_plan** out);
+int hd_plan_destroy(hd_plan* plan);
+/* Device pointer of a workspace buffer (HD_BUF_*). */
+void* hd_plan_buffer(hd_plan* plan, int which);
+int64_t hd_plan_total_points(const hd_plan* plan);
+
+/* ---- field-level operators (reference public API) -------------------------- */
+
+/* grid.py:236-251 fill_ghosts_periodic / fill_ghosts_array: periodic wrap of
+ * `nfields` consecutive fields along the plan's locally periodic axes. */
+int hd_fill_ghosts(hd_plan* plan, double* fields, int nfields, void* stream);
+
+/* kernels.py:68-204 hyper_sweep over every interior line along `dim`, with the
+ * flux components of upwind.py:116-127 formed on the fly from u.
+ * accumulate=1: inc -= dF/dx; accumulate=0: inc = 0 - dF/dx (interior only). */
+int hd_hyper_sweep(hd_plan* plan, int dim, const double* u, double* inc, int accumulate,
+                   void* stream);
+
+/* upwind.py:163-213 hyperbolic_rhs: x, y, z sweeps; also latches positivity. */
+int hd_hyperbolic_rhs(hd_plan* plan, const double* u, double* inc, int accumulate, void* stream);
+
+/* viscous.py:54-121 parabolic_rhs: accumulates into inc rows 1..4. */
+int hd_parabolic_rhs(hd_plan* plan, const double* u, double* inc, void* stream);
+
+/* kernels.py:207-227 central_diff4, same argument list. */
+int hd_central_diff4(const double* src, double* dst, int di, int dj, int dk, int g, int og,
+                     int nx, int ny, int nz, int k_lo, int k_hi, double coef, void* stream);
+
+/* timeint.py:152-156 rhs(u): ghost fill of u, then hyperbolic + parabolic into inc. */
+int hd_rhs(hd_plan* plan, double* u, double* inc, void* stream);
+
+/* ---- steppers --------------------------------------------------------------- */
+
+/* One full step (timeint.py:181-193 rk4_step / 168-178 rk3_tvd_step), u in
+ * place, dt read from device memory.  Ghosts of u must be valid on entry and
+ * are valid on exit (locally periodic axes).  `tag` identifies the step in
+ * the error key. */
+int hd_step(hd_plan* plan, int scheme, double* u, const double* dt_dev, int64_t tag,
+            void* stream);
+
+/* One part of one RK stage (decomposed runs).  Stage s reads u (s == 0) or
+ * the workspace STAGE buffer; the UPDATE part writes the next stage state
+ * (or u itself after the last stage). */
+int hd_stage_part(hd_plan* plan, int scheme, int stage, int parts, double* u,
+                  const double* dt_dev, int64_t tag, void* stream);
+
+/* ---- reductions and step bookkeeping --------------------------------------- */
+
+/* timeint.py:100-131: one pass over the interior producing HD_RED_* results
+ * at `out` (device, HD_RED_N doubles).  Latches positivity (cons_to_prim). */
+int hd_reduce_state(hd_plan* plan, const double* u, double* out, int64_t tag, void* stream);
+
+/* timeint.py:133-138 + 224-237: ctx[DT] = cfl / signal (cfl > 0) or dt_fixed,
+ * clipped to t_final - ctx[T] when t_final >= 0.  Latches a zero/non-finite
+ * signal.  signal = red[HD_RED_SIGNAL_MAX] or [SUM] per cfl_mode (0/1). */
+int hd_set_dt(hd_plan* plan, const double* red, int cfl_mode, double cfl, double dt_fixed,
+              double t_final, double* ctx, int64_t tag, void* stream);
+/* ctx[T] += ctx[DT] */
+int hd_commit_time(hd_plan* plan, double* ctx, void* stream);
+
+/* ---- errors ----------------------------------------------------------------- */
+
+/* Error key: 0 = none, else (tag << 36) | (code << 34) | flat point index;
+ * the smallest key wins (earliest tag, density before pressure, lowest index).
+ * code 1 = nonpositive density, 2 = nonpositive pressure, 3 = bad CFL signal.
+ * tag = step * 8 + slot: hd_step/hd_stage_part latch slot 1 + stage with
+ * their `tag` argument as the step; hd_reduce_state / hd_set_dt latch their
+ * `tag` verbatim (callers use slot 0 before a step, 7 after it). */
+int hd_error_read(hd_plan* plan, uint64_t* key, void* stream);
+int hd_error_clear(hd_plan* plan, void* stream);
+
+/* Kernels launched by this library since load (monotonic; for launch accounting). */
+int64_t hd_launch_counter(void);
+
+/* ---- microbenchmark ---------------------------------------------------------- */
+/* FP64 FMA throughput probe: iters DFMA per thread on `out` (blocks x threads). */
+int hd_fp64_probe(double* out, int blocks, int threads, int iters, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HD_H_ */

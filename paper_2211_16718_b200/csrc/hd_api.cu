@@ -1,0 +1,295 @@
+// hd_api.cu -- extern "C" boundary of libhd.so (declared in include/hd.h).
+//
+// The reference's seams this boundary replaces (pkg/src/hitdns/):
+//   hd_hyper_sweep     kernels.py:68-73   hyper_sweep(u, f, inc, ...)
+//   hd_central_diff4   kernels.py:207-208 central_diff4(src, dst, ...)
+//   hd_hyperbolic_rhs  upwind.py:163-170  hyperbolic_rhs(fields, gas, params, delta, workers, out)
+//   hd_parabolic_rhs   viscous.py:54-60   parabolic_rhs(fields, gas, halo, workers, out)
+//   hd_rhs             timeint.py:141-158 make_rhs(...) -> rhs(fields)
+//   hd_step            timeint.py:168-193 rk3_tvd_step / rk4_step (STEPPERS, :196)
+//   hd_stage_part      the same stages split around the halo seam grid.py:254-267 /
+//                      decomp.py:183-241 (sync_fields / sync_scalars)
+//   hd_reduce_state    timeint.py:100-131 conserved_totals / max_wavespeed_interior / max_signal
+//   hd_set_dt          timeint.py:133-138 compute_dt + the t_final clip of :236-237
+//   hd_fill_ghosts     grid.py:236-251    fill_ghosts_periodic / fill_ghosts_array
+#include <atomic>
+#include <cstring>
+#include <new>
+
+#include "hd_internal.cuh"
+
+using namespace hd;
+
+namespace {
+
+std::atomic<int64_t> g_launches{0};
+int64_t hd_launches_total() { return g_launches.load(); }
+
+constexpr int64_t ALIGN = 256;
+constexpr int64_t RED_BYTES = (2048 * 9 + 16) * 8;
+
+int64_t align_up(int64_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+bool geom_ok(const hd_geom* g) {
+  if (!g || g->ghost < 3) return false;
+  for (int d = 0; d < 3; ++d) {
+    if (g->n[d] < 1 || !(g->length[d] > 0.0)) return false;
+    if (g->n[d] < g->ghost) return false;  // decomp.py:78-82 (local extent >= ghost width)
+  }
+  return true;
+}
+
+int64_t npts_of(const hd_geom* g) {
+  return (int64_t)(g->n[0] + 2 * g->ghost) * (g->n[1] + 2 * g->ghost) * (g->n[2] + 2 * g->ghost);
+}
+
+void layout(const hd_geom* g, int64_t off[HD_NBUF], int64_t* total) {
+  const int64_t f = npts_of(g) * 8;
+  int64_t o = 0;
+  const int64_t sizes[HD_NBUF] = {5 * f, 5 * f, 5 * f, 4 * f, 12 * f, RED_BYTES, 8 * HD_CTX_N, 64};
+  for (int b = 0; b < HD_NBUF; ++b) {
+    off[b] = o;
+    o = align_up(o + sizes[b]);
+  }
+  *total = o;
+}
+
+cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+double* buf(hd_plan* p, int which) { return (double*)(p->ws + p->off[which]); }
+
+// exchanged axes must be a suffix (z, or y+z) so the exact accumulation order
+// x, y, z of upwind.py:200 is kept when the local sweeps run first
+bool parts_supported(const hd_plan* p) {
+  const int* per = p->geo.periodic;
+  if (!per[0] && (per[1] || per[2])) return false;
+  if (!per[1] && per[2]) return false;
+  return true;
+}
+
+int mask_of(const hd_plan* p, bool periodic) {
+  int m = 0;
+  for (int d = 0; d < 3; ++d)
+    if ((p->geo.periodic[d] != 0) == periodic) m |= 1 << d;
+  return m;
+}
+
+// sweeps for the dims in `dmask`, in x, y, z order; the first sweep of the
+// RHS overwrites inc (0 - d, upwind.py:181-182) unless `accumulate_first`.
+int sweeps(hd_plan* p, int dmask, const double* us, double* inc, bool first_overwrites, int64_t tag,
+           cudaStream_t s) {
+  bool first = first_overwrites;
+  for (int d = 0; d < 3; ++d) {
+    if (!(dmask & (1 << d))) continue;
+    int rc = launch_sweep(p, d, us, inc, first ? 0 : 1, d == 0 ? 1 : 0, tag, s);
+    if (rc) return rc;
+    first = false;
+  }
+  return HD_OK;
+}
+
+int nstages(int scheme) { return scheme == HD_SCHEME_RK3 ? 3 : 4; }
+
+}  // namespace
+
+extern "C" {
+
+int hd_abi_version(void) { return HD_ABI_VERSION; }
+
+int64_t hd_launch_counter(void) { return hd_launches_total(); }
+
+const char* hd_status_string(int status) {
+  switch (status) {
+    case HD_OK: return "ok";
+    case HD_E_ARG: return "invalid argument";
+    case HD_E_CUDA: return "CUDA error";
+    case HD_E_WORKSPACE: return "workspace missing or too small";
+    case HD_E_UNSUPPORTED: return "unsupported configuration";
+    default: return "unknown status";
+  }
+}
+
+int64_t hd_workspace_bytes(const hd_geom* geom) {
+  if (!geom_ok(geom)) return HD_E_ARG;
+  int64_t off[HD_NBUF], total;
+  layout(geom, off, &total);
+  return total;
+}
+
+int hd_plan_create(const hd_geom* geom, const hd_gas* gas, const hd_weno* weno, int mode,
+                   void* workspace, int64_t workspace_bytes, hd_plan** out) {
+  if (!out) return HD_E_ARG;
+  *out = nullptr;
+  if (!geom_ok(geom) || !gas || !weno) return HD_E_ARG;
+  if (!(gas->gamma > 1.0) || !(gas->prandtl > 0.0) || gas->mu < 0.0) return HD_E_ARG;
+  if (!(weno->epsilon > 0.0) || weno->power < 1) return HD_E_ARG;
+  if (mode != HD_MODE_FAST && mode != HD_MODE_EXACT) return HD_E_ARG;
+  int64_t off[HD_NBUF], total;
+  layout(geom, off, &total);
+  // workspace == NULL: geometry-only plan (ghost fills); compute calls then fail
+  if (workspace && (workspace_bytes < total || ((uintptr_t)workspace % ALIGN))) return HD_E_WORKSPACE;
+  hd_plan* p = new (std::nothrow) hd_plan;
+  if (!p) return HD_E_ARG;
+  std::memset(p, 0, sizeof(*p));
+  p->geom = *geom;
+  p->gas = *gas;
+  p->weno = *weno;
+  p->mode = mode;
+  Geo& G = p->geo;
+  G.g = geom->ghost;
+  for (int d = 0; d < 3; ++d) {
+    G.n[d] = geom->n[d];
+    G.gn[d] = geom->n[d] + 2 * geom->ghost;
+    G.h[d] = geom->length[d] / (double)geom->n[d];  // grid.py:73-74
+    G.periodic[d] = geom->periodic[d] ? 1 : 0;
+  }
+  G.npts = npts_of(geom);
+  G.sy = G.gn[0];
+  G.sz = (int64_t)G.gn[0] * G.gn[1];
+  Phys& ph = p->phys;
+  ph.gamma = gas->gamma;
+  ph.gm1 = gas->gamma - 1.0;
+  ph.prandtl = gas->prandtl;
+  ph.mu = gas->mu * gas->visc_scale;  // physics.py:42-44 effective_mu
+  ph.eps = weno->epsilon;
+  ph.power = weno->power;
+  ph.delta = weno->delta;
+  p->ws = (char*)workspace;
+  p->ws_bytes = workspace_bytes;
+  std::memcpy(p->off, off, sizeof(off));
+  if (cudaGetDevice(&p->device) != cudaSuccess ||
+      cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {
+    delete p;
+    return HD_E_CUDA;
+  }
+  // error key starts at "none"; context zeroed
+  if (p->ws && (cudaMemset(p->ws + p->off[HD_BUF_ERR], 0xff, 8) != cudaSuccess ||
+      cudaMemset(p->ws + p->off[HD_BUF_CTX], 0, 8 * HD_CTX_N) != cudaSuccess)) {
+    delete p;
+    return HD_E_CUDA;
+  }
+  *out = p;
+  return HD_OK;
+}
+
+int hd_plan_destroy(hd_plan* p) {
+  delete p;
+  return HD_OK;
+}
+
+void* hd_plan_buffer(hd_plan* p, int which) {
+  if (!p || !p->ws || which < 0 || which >= HD_NBUF) return nullptr;
+  return p->ws + p->off[which];
+}
+
+int64_t hd_plan_total_points(const hd_plan* p) { return p ? p->geo.npts : HD_E_ARG; }
+
+int hd_fill_ghosts(hd_plan* p, double* fields, int nfields, void* stream) {
+  if (!p || !fields || nfields < 1) return HD_E_ARG;
+  return launch_fill_ghosts(p, fields, nfields, 7, S(stream));
+}
+
+int hd_hyper_sweep(hd_plan* p, int dim, const double* u, double* inc, int accumulate, void* stream) {
+  if (!p || !u || !inc || dim < 0 || dim > 2) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  return launch_sweep(p, dim, u, inc, accumulate ? 1 : 0, 0, 0, S(stream));
+}
+
+int hd_hyperbolic_rhs(hd_plan* p, const double* u, double* inc, int accumulate, void* stream) {
+  if (!p || !u || !inc) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  return sweeps(p, 7, u, inc, !accumulate, 0, S(stream));
+}
+
+int hd_parabolic_rhs(hd_plan* p, const double* u, double* inc, void* stream) {
+  if (!p || !u || !inc) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  if (p->phys.mu == 0.0) return HD_OK;  // viscous.py:72-73
+  if (!parts_supported(p)) return HD_E_UNSUPPORTED;
+  int rc = launch_prims(p, u, S(stream));
+  if (!rc) rc = launch_gradflux(p, S(stream));
+  if (!rc) rc = launch_divergence(p, 7, inc, inc, 0, HD_SCHEME_RK4, 0, nullptr, nullptr, S(stream));
+  return rc;
+}
+
+int hd_rhs(hd_plan* p, double* u, double* inc, void* stream) {
+  if (!p || !u || !inc) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  int rc = launch_fill_ghosts(p, u, 5, 7, S(stream));
+  if (!rc) rc = sweeps(p, 7, u, inc, true, 0, S(stream));
+  if (!rc) rc = hd_parabolic_rhs(p, u, inc, stream);
+  return rc;
+}
+
+int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const double* dt_dev,
+                  int64_t tag, void* stream) {
+  if (!p || !u || (scheme != HD_SCHEME_RK3 && scheme != HD_SCHEME_RK4)) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  if (stage < 0 || stage >= nstages(scheme)) return HD_E_ARG;
+  if (!parts_supported(p)) return HD_E_UNSUPPORTED;
+  cudaStream_t s = S(stream);
+  const double* us = stage == 0 ? u : buf(p, HD_BUF_STAGE);
+  double* inc = buf(p, HD_BUF_INC);
+  const int loc = mask_of(p, true), ex = mask_of(p, false);
+  const bool visc = p->phys.mu != 0.0;
+  const int64_t t = tag * 8 + 1 + stage;  // slot 1..4: RK stage (0 = pre-step CFL, 7 = diagnostics)
+  int rc = HD_OK;
+  if ((parts & HD_PART_LOCAL) && loc) rc = sweeps(p, loc, us, inc, true, t, s);
+  if (!rc && (parts & HD_PART_HALO)) {
+    if (ex) rc = sweeps(p, ex, us, inc, loc == 0, t, s);
+    if (!rc && visc) rc = launch_prims(p, us, s);
+    if (!rc && visc) rc = launch_gradflux(p, s);
+  }
+  if (!rc && (parts & HD_PART_DIVLOC) && visc && ex && loc)
+    rc = launch_divergence(p, loc, inc, inc, 0, scheme, stage, nullptr, nullptr, s);
+  if (!rc && (parts & HD_PART_UPDATE)) {
+    if (!dt_dev) return HD_E_ARG;
+    // with no exchanged axis the whole divergence happens here (single fused pass)
+    const int dmask = visc ? (ex ? ex : 7) : 0;
+    rc = launch_divergence(p, dmask, inc, nullptr, 1, scheme, stage, u, dt_dev, s);
+  }
+  return rc;
+}
+
+int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag, void* stream) {
+  if (!p || !u || !dt_dev) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  if (scheme != HD_SCHEME_RK3 && scheme != HD_SCHEME_RK4) return HD_E_ARG;
+  for (int d = 0; d < 3; ++d)
+    if (!p->geo.periodic[d]) return HD_E_UNSUPPORTED;  // decomposed runs use hd_stage_part
+  // timeint.py:153: the rhs syncs the ghosts of its input first
+  int rc = launch_fill_ghosts(p, u, 5, 7, S(stream));
+  for (int st = 0; st < nstages(scheme) && !rc; ++st)
+    rc = hd_stage_part(p, scheme, st, HD_PART_ALL, u, dt_dev, tag, stream);
+  return rc;
+}
+
+int hd_reduce_state(hd_plan* p, const double* u, double* out, int64_t tag, void* stream) {
+  if (!p || !u || !out) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  return launch_reduce(p, u, out, tag, S(stream));
+}
+
+int hd_error_read(hd_plan* p, uint64_t* key, void* stream) {
+  if (!p || !key) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  unsigned long long v = 0;
+  if (cudaMemcpyAsync(&v, p->ws + p->off[HD_BUF_ERR], 8, cudaMemcpyDeviceToHost, S(stream)) != cudaSuccess ||
+      cudaStreamSynchronize(S(stream)) != cudaSuccess)
+    return HD_E_CUDA;
+  *key = (v == ~0ull) ? 0 : (uint64_t)v;
+  return HD_OK;
+}
+
+int hd_error_clear(hd_plan* p, void* stream) {
+  if (!p) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  return cudaMemsetAsync(p->ws + p->off[HD_BUF_ERR], 0xff, 8, S(stream)) == cudaSuccess ? HD_OK
+                                                                                        : HD_E_CUDA;
+}
+
+}  // extern "C"
+
+namespace hd {
+void count_launches(int n) { g_launches += n; }
+}  // namespace hd

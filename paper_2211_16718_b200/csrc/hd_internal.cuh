@@ -1,0 +1,112 @@
+// hd_internal.cuh -- shared definitions of the libhd.so kernels (sm_100a).
+//
+// Arithmetic policies
+//   EXACT: every operation is an explicit IEEE round-to-nearest intrinsic
+//          (__dadd_rn/__dmul_rn/__ddiv_rn/__dsqrt_rn: never contracted into
+//          DFMA) in the reference's association order, so results are
+//          bitwise equal to the numba/numpy reference.
+//   FAST:  algebraically rearranged (shared smoothness indicators, one
+//          reciprocal per reconstruction pair, rsqrt-based Roe averages,
+//          DFMA contraction).  Parity bar: 1e-10 relative L2 per conserved
+//          variable after N steps (BASELINE.json north_star).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hd.h"
+
+namespace hd {
+
+constexpr int NV = 5;
+
+// weno.py:28-33 literals (Python doubles; constant-folded identically).
+constexpr double C13_12 = 13.0 / 12.0;
+constexpr double C1_3 = 1.0 / 3.0;
+constexpr double C7_6 = 7.0 / 6.0;
+constexpr double C11_6 = 11.0 / 6.0;
+constexpr double C1_6 = 1.0 / 6.0;
+constexpr double C5_6 = 5.0 / 6.0;
+
+// ---- exact IEEE primitives (never fused) --------------------------------------
+__device__ __forceinline__ double xa(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xs(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xd(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double xsqrt(double a) { return __dsqrt_rn(a); }
+
+// ---- fast reciprocal: MUFU.RCP64H seed + two Newton steps (~1 ulp) ----------
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Geometry of one plan, passed by value to every kernel.
+struct Geo {
+  int n[3];     // interior extents (x, y, z)
+  int gn[3];    // ghosted extents
+  int g;
+  int64_t npts; // ghosted points per field
+  int64_t sy, sz;  // strides of y and z in points (sx = 1)
+  double h[3];  // spacing
+  int periodic[3];
+
+  __host__ __device__ int64_t idx(int i, int j, int k) const {  // interior coords, may be in ghosts
+    return ((int64_t)(k + g) * gn[1] + (j + g)) * gn[0] + (i + g);
+  }
+  __host__ __device__ int64_t stride(int d) const { return d == 0 ? 1 : (d == 1 ? sy : sz); }
+};
+
+struct Phys {
+  double gamma, gm1, prandtl, mu;  // mu = effective viscosity (mu * visc_scale)
+  double eps, delta;
+  int power;
+};
+
+// Error latch: key = (tag << 36) | (code << 34) | point, min wins; ~0 = none.
+__device__ __forceinline__ void latch_error(unsigned long long* key, int64_t tag, int code,
+                                            int64_t point) {
+  unsigned long long v = ((unsigned long long)tag << 36) | ((unsigned long long)code << 34) |
+                         ((unsigned long long)point & ((1ull << 34) - 1));
+  atomicMin(key, v);
+}
+
+}  // namespace hd
+
+// Host-side plan (opaque to C callers).
+struct hd_plan {
+  hd_geom geom;
+  hd_gas gas;
+  hd_weno weno;
+  int mode;
+  hd::Geo geo;
+  hd::Phys phys;
+  char* ws;
+  int64_t ws_bytes;
+  int64_t off[HD_NBUF];
+  int device;
+  int sm_count;
+};
+
+namespace hd {
+// number of kernels this library has launched (hd_launch_counter)
+void count_launches(int n);
+// launchers implemented in the .cu files
+int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int accumulate,
+                 int check, int64_t tag, cudaStream_t s);
+int launch_fill_ghosts(const hd_plan* p, double* f, int nfields, int axis_mask, cudaStream_t s);
+int launch_prims(const hd_plan* p, const double* u, cudaStream_t s);
+int launch_gradflux(const hd_plan* p, cudaStream_t s);
+// divergence (+ optional RK update).  dims_mask: which d's divergence to add;
+// update: 0 = store inc, else RK stage update with scheme/stage.
+int launch_divergence(const hd_plan* p, int dims_mask, const double* inc_in, double* inc_out,
+                      int update, int scheme, int stage, double* u, const double* dt_dev,
+                      cudaStream_t s);
+int launch_rk_update(const hd_plan* p, const double* inc, int scheme, int stage, double* u,
+                     const double* dt_dev, cudaStream_t s);
+int launch_reduce(const hd_plan* p, const double* u, double* out, int64_t tag, cudaStream_t s);
+}  // namespace hd

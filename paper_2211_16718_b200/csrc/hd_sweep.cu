@@ -1,0 +1,458 @@
+// hd_sweep.cu -- fused WENO5 (state + flux) / Roe / flux-difference sweeps.
+//
+// Replaces kernels.py:68-204 (hyper_sweep) together with the flux arrays
+// upwind.py:116-127 (_flux_components) that the reference materialises per
+// dimension: here f(u) is formed on the fly when a point enters the window.
+//
+// Execution model: one thread marches one segment [c0, c1) of one grid line
+// along the sweep axis, holding a 5-point register window of the state and
+// flux (u0..u4, f1..f4; f0 == u_{1+dim}).  At cell c the window (c-2..c+2)
+// yields the RIGHT reconstruction at c-1/2 and the LEFT reconstruction at
+// c+1/2 (the reference's mirrored stencils, K:104-123, share this window), so
+// each window is evaluated once and each interface flux once (the reference's
+// fprev carry, K:197-203).  The Roe flux at c-1/2 combines the carried left
+// state with the fresh right state.
+//
+// y/z sweeps: lanes are consecutive x columns -> every window load and every
+// inc read-modify-write is a fully coalesced 256-byte warp access.
+// x sweep: lanes are consecutive y rows; each lane walks its row sequentially
+// (sector reuse through L1).
+#include "hd_internal.cuh"
+
+namespace hd {
+
+// ---------------------------------------------------------------------------
+// WENO5 reconstructions
+// ---------------------------------------------------------------------------
+
+// kernels.py:25-57, exact operation order.
+__device__ __forceinline__ double recon5_exact(double f0, double f1, double f2, double f3,
+                                               double f4, double eps, int power) {
+  const double t1 = xa(xs(f0, xm(2.0, f1)), f2);
+  const double s1 = xa(xs(f0, xm(4.0, f1)), xm(3.0, f2));
+  const double b1 = xa(xm(C13_12, xm(t1, t1)), xm(0.25, xm(s1, s1)));
+  const double t2 = xa(xs(f1, xm(2.0, f2)), f3);
+  const double s2 = xs(f1, f3);
+  const double b2 = xa(xm(C13_12, xm(t2, t2)), xm(0.25, xm(s2, s2)));
+  const double t3 = xa(xs(f2, xm(2.0, f3)), f4);
+  const double s3 = xa(xs(xm(3.0, f2), xm(4.0, f3)), f4);
+  const double b3 = xa(xm(C13_12, xm(t3, t3)), xm(0.25, xm(s3, s3)));
+  const double d1 = xa(eps, b1), d2 = xa(eps, b2), d3 = xa(eps, b3);
+  double e1 = d1, e2 = d2, e3 = d3;
+  for (int q = 0; q < power - 1; ++q) {
+    e1 = xm(e1, d1);
+    e2 = xm(e2, d2);
+    e3 = xm(e3, d3);
+  }
+  const double a1 = xd(0.1, e1), a2 = xd(0.6, e2), a3 = xd(0.3, e3);
+  const double asum = xa(xa(a1, a2), a3);
+  const double w1 = xd(a1, asum), w2 = xd(a2, asum), w3 = xd(a3, asum);
+  const double c1 = xa(xs(xm(C1_3, f0), xm(C7_6, f1)), xm(C11_6, f2));
+  const double c2 = xa(xa(xm(-C1_6, f1), xm(C5_6, f2)), xm(C1_3, f3));
+  const double c3 = xs(xa(xm(C1_3, f2), xm(C5_6, f3)), xm(C1_6, f4));
+  return xa(xa(xm(w1, c1), xm(w2, c2)), xm(w3, c3));
+}
+
+// Both reconstructions of one 5-point window q0..q4 (centred on cell c):
+//   left  = value at c+1/2 (stencil q0..q4),
+//   right = value at c-1/2 (mirrored stencil q4..q0).
+// The mirrored stencil has the same smoothness indicators in reverse order
+// (weno.py:9-11), so beta/eps terms are computed once; the three normalised
+// weights of each side share one reciprocal:
+//   w_k = (g_k / e_k) / sum_j (g_j / e_j) = g_k prod_{j!=k} e_j / sum_j g_j prod_{i!=j} e_i.
+template <bool EXACT>
+__device__ __forceinline__ void recon_pair(double q0, double q1, double q2, double q3, double q4,
+                                           double eps, int power, double& left, double& right) {
+  if constexpr (EXACT) {
+    left = recon5_exact(q0, q1, q2, q3, q4, eps, power);
+    right = recon5_exact(q4, q3, q2, q1, q0, eps, power);
+  } else {
+    const double t1 = (q0 - 2.0 * q1) + q2;
+    const double s1 = (q0 - 4.0 * q1) + 3.0 * q2;
+    const double t2 = (q1 - 2.0 * q2) + q3;
+    const double s2 = q1 - q3;
+    const double t3 = (q2 - 2.0 * q3) + q4;
+    const double s3 = (3.0 * q2 - 4.0 * q3) + q4;
+    const double d1 = fma(C13_12 * t1, t1, fma(0.25 * s1, s1, eps));
+    const double d2 = fma(C13_12 * t2, t2, fma(0.25 * s2, s2, eps));
+    const double d3 = fma(C13_12 * t3, t3, fma(0.25 * s3, s3, eps));
+    double e1 = d1, e2 = d2, e3 = d3;
+    for (int q = 0; q < power - 1; ++q) {
+      e1 *= d1;
+      e2 *= d2;
+      e3 *= d3;
+    }
+    const double e12 = e1 * e2, e13 = e1 * e3, e23 = e2 * e3;
+    const double mid = 6.0 * e13;  // 0.6/e2 weight, both sides (x10 scaling cancels)
+    // left: (0.1/e1, 0.6/e2, 0.3/e3) ~ (e23, 6 e13, 3 e12)
+    const double nl1 = e23, nl3 = 3.0 * e12;
+    const double cl1 = fma(C11_6, q2, fma(C1_3, q0, -C7_6 * q1));
+    const double cl2 = fma(C1_3, q3, fma(C5_6, q2, -C1_6 * q1));
+    const double cl3 = fma(C1_3, q2, fma(C5_6, q3, -C1_6 * q4));
+    left = fma(nl1, cl1, fma(mid, cl2, nl3 * cl3)) * frcp((nl1 + mid) + nl3);
+    // right (mirrored): (0.1/e3, 0.6/e2, 0.3/e1) ~ (e12, 6 e13, 3 e23)
+    const double nr1 = e12, nr3 = 3.0 * e23;
+    const double cr1 = fma(C11_6, q2, fma(C1_3, q4, -C7_6 * q3));
+    const double cr2 = fma(C1_3, q1, fma(C5_6, q2, -C1_6 * q3));
+    const double cr3 = fma(C1_3, q2, fma(C5_6, q1, -C1_6 * q0));
+    right = fma(nr1, cr1, fma(mid, cr2, nr3 * cr3)) * frcp((nr1 + mid) + nr3);
+  }
+}
+
+// kernels.py:60-65
+template <bool EXACT>
+__device__ __forceinline__ double entropy_fixed(double lam, double delta) {
+  const double mag = fabs(lam);
+  if (delta > 0.0 && mag < delta) {
+    if constexpr (EXACT) return xd(xa(xm(lam, lam), xm(delta, delta)), xm(2.0, delta));
+    return (lam * lam + delta * delta) / (2.0 * delta);
+  }
+  return mag;
+}
+
+// ---------------------------------------------------------------------------
+// Roe interface flux (kernels.py:125-195)
+// ---------------------------------------------------------------------------
+template <int DIM, bool EXACT>
+__device__ __forceinline__ void roe_flux(const double (&uL)[NV], const double (&uR)[NV],
+                                         const double (&fl)[NV], const double (&fr)[NV],
+                                         const Phys& ph, double (&flux)[NV]) {
+  constexpr int mn = 1 + DIM, mt1 = 1 + (DIM + 1) % 3, mt2 = 1 + (DIM + 2) % 3;
+  const double gm1 = ph.gm1;
+  if constexpr (EXACT) {
+    const double rl = uL[0];
+    const double il = xd(1.0, rl);
+    const double vxl = xm(uL[1], il), vyl = xm(uL[2], il), vzl = xm(uL[3], il);
+    const double pl = xm(gm1, xs(uL[4], xm(xm(0.5, rl), xa(xa(xm(vxl, vxl), xm(vyl, vyl)), xm(vzl, vzl)))));
+    const double rr = uR[0];
+    const double ir = xd(1.0, rr);
+    const double vxr = xm(uR[1], ir), vyr = xm(uR[2], ir), vzr = xm(uR[3], ir);
+    const double pr = xm(gm1, xs(uR[4], xm(xm(0.5, rr), xa(xa(xm(vxr, vxr), xm(vyr, vyr)), xm(vzr, vzr)))));
+    const double sl = xsqrt(rl), sr = xsqrt(rr);
+    const double isw = xd(1.0, xa(sl, sr));
+    const double ua = xm(xa(xm(sl, vxl), xm(sr, vxr)), isw);
+    const double va = xm(xa(xm(sl, vyl), xm(sr, vyr)), isw);
+    const double wa = xm(xa(xm(sl, vzl), xm(sr, vzr)), isw);
+    const double Hl = xm(xa(uL[4], pl), il);
+    const double Hr = xm(xa(uR[4], pr), ir);
+    const double Ha = xm(xa(xm(sl, Hl), xm(sr, Hr)), isw);
+    const double q2 = xa(xa(xm(ua, ua), xm(va, va)), xm(wa, wa));
+    const double a2 = xm(gm1, xs(Ha, xm(0.5, q2)));
+    const double aa = xsqrt(a2);
+    double vn, vt1, vt2;
+    if (DIM == 0) { vn = ua; vt1 = va; vt2 = wa; }
+    else if (DIM == 1) { vn = va; vt1 = wa; vt2 = ua; }
+    else { vn = wa; vt1 = ua; vt2 = va; }
+    const double dr = xs(uR[0], uL[0]);
+    const double dmn = xs(uR[mn], uL[mn]);
+    const double dt1 = xs(uR[mt1], uL[mt1]);
+    const double dt2 = xs(uR[mt2], uL[mt2]);
+    const double dE = xs(uR[4], uL[4]);
+    const double b1 = xd(gm1, a2);
+    const double b2 = xm(xm(0.5, b1), q2);
+    const double ia = xd(1.0, aa);
+    const double b1vt1dt1 = xm(xm(b1, vt1), dt1), b1vt2dt2 = xm(xm(b1, vt2), dt2);
+    const double b1dE = xm(b1, dE);
+    const double s1 = xm(0.5, xa(xs(xs(xs(xm(xa(b2, xm(vn, ia)), dr), xm(xa(xm(b1, vn), ia), dmn)),
+                                       b1vt1dt1), b1vt2dt2), b1dE));
+    const double s2 = xs(xa(xa(xa(xm(xs(1.0, b2), dr), xm(xm(b1, vn), dmn)), b1vt1dt1), b1vt2dt2), b1dE);
+    const double s3 = xa(xm(-vt1, dr), dt1);
+    const double s4 = xa(xm(-vt2, dr), dt2);
+    const double s5 = xm(0.5, xa(xs(xs(xs(xm(xs(b2, xm(vn, ia)), dr), xm(xs(xm(b1, vn), ia), dmn)),
+                                       b1vt1dt1), b1vt2dt2), b1dE));
+    const double lam_n = entropy_fixed<true>(vn, ph.delta);
+    const double k1 = xm(entropy_fixed<true>(xs(vn, aa), ph.delta), s1);
+    const double k2 = xm(lam_n, s2);
+    const double k3 = xm(lam_n, s3);
+    const double k4 = xm(lam_n, s4);
+    const double k5 = xm(entropy_fixed<true>(xa(vn, aa), ph.delta), s5);
+    const double diss_r = xa(xa(k1, k2), k5);
+    const double diss_n = xa(xa(xm(k1, xs(vn, aa)), xm(k2, vn)), xm(k5, xa(vn, aa)));
+    const double diss_1 = xa(xa(xa(xm(k1, vt1), xm(k2, vt1)), k3), xm(k5, vt1));
+    const double diss_2 = xa(xa(xa(xm(k1, vt2), xm(k2, vt2)), k4), xm(k5, vt2));
+    const double diss_E = xa(xa(xa(xa(xm(k1, xs(Ha, xm(vn, aa))), xm(k2, xm(0.5, q2))), xm(k3, vt1)),
+                                xm(k4, vt2)), xm(k5, xa(Ha, xm(vn, aa))));
+    flux[0] = xs(xm(0.5, xa(fl[0], fr[0])), xm(0.5, diss_r));
+    flux[1] = xm(0.5, xa(fl[1], fr[1]));
+    flux[2] = xm(0.5, xa(fl[2], fr[2]));
+    flux[3] = xm(0.5, xa(fl[3], fr[3]));
+    flux[4] = xs(xm(0.5, xa(fl[4], fr[4])), xm(0.5, diss_E));
+    flux[mn] = xs(flux[mn], xm(0.5, diss_n));
+    flux[mt1] = xs(flux[mt1], xm(0.5, diss_1));
+    flux[mt2] = xs(flux[mt2], xm(0.5, diss_2));
+  } else {
+    // rsqrt-based: 1/rho = (rho^-1/2)^2, sqrt(rho) = rho * rho^-1/2
+    const double rl = uL[0], rr = uR[0];
+    const double isl = rsqrt(rl), isr = rsqrt(rr);
+    const double il = isl * isl, ir = isr * isr;
+    const double sl = rl * isl, sr = rr * isr;
+    // kinetic energy 0.5*rho*|v|^2 = 0.5*|m|^2/rho
+    const double pl = gm1 * (uL[4] - (0.5 * il) * (uL[1] * uL[1] + uL[2] * uL[2] + uL[3] * uL[3]));
+    const double pr = gm1 * (uR[4] - (0.5 * ir) * (uR[1] * uR[1] + uR[2] * uR[2] + uR[3] * uR[3]));
+    const double isw = frcp(sl + sr);
+    // sl*v_l = m_l * isl (since m = rho v): saves the velocity products
+    const double ua = (uL[1] * isl + uR[1] * isr) * isw;
+    const double va = (uL[2] * isl + uR[2] * isr) * isw;
+    const double wa = (uL[3] * isl + uR[3] * isr) * isw;
+    // sl*H_l = (E_l + p_l) * isl
+    const double Ha = ((uL[4] + pl) * isl + (uR[4] + pr) * isr) * isw;
+    const double q2 = ua * ua + va * va + wa * wa;
+    const double a2 = gm1 * (Ha - 0.5 * q2);
+    const double ia = rsqrt(a2);
+    const double aa = a2 * ia;
+    double vn, vt1, vt2;
+    if (DIM == 0) { vn = ua; vt1 = va; vt2 = wa; }
+    else if (DIM == 1) { vn = va; vt1 = wa; vt2 = ua; }
+    else { vn = wa; vt1 = ua; vt2 = va; }
+    const double dr = uR[0] - uL[0];
+    const double dmn = uR[mn] - uL[mn];
+    const double dt1 = uR[mt1] - uL[mt1];
+    const double dt2 = uR[mt2] - uL[mt2];
+    const double dE = uR[4] - uL[4];
+    const double b1 = gm1 * (ia * ia);
+    const double b2 = 0.5 * b1 * q2;
+    // common part of s1/s5: b2*dr - b1*(vn*dmn + vt1*dt1 + vt2*dt2 - dE)
+    const double proj = vn * dmn + vt1 * dt1 + vt2 * dt2 - dE;
+    const double common = b2 * dr - b1 * proj;
+    const double acoustic = ia * (vn * dr - dmn);
+    const double s1 = 0.5 * (common + acoustic);
+    const double s5 = 0.5 * (common - acoustic);
+    const double s2 = dr - common;  // (1-b2) dr + b1 (vn dmn + vt1 dt1 + vt2 dt2) - b1 dE
+    const double s3 = dt1 - vt1 * dr;
+    const double s4 = dt2 - vt2 * dr;
+    const double lam_n = entropy_fixed<false>(vn, ph.delta);
+    const double k1 = entropy_fixed<false>(vn - aa, ph.delta) * s1;
+    const double k2 = lam_n * s2;
+    const double k3 = lam_n * s3;
+    const double k4 = lam_n * s4;
+    const double k5 = entropy_fixed<false>(vn + aa, ph.delta) * s5;
+    const double k15 = k1 + k5;
+    const double k125 = k15 + k2;
+    const double diss_r = k125;
+    const double diss_n = k125 * vn + (k5 - k1) * aa;
+    const double diss_1 = k125 * vt1 + k3;
+    const double diss_2 = k125 * vt2 + k4;
+    const double diss_E = k15 * Ha + (k5 - k1) * (vn * aa) + k2 * (0.5 * q2) + k3 * vt1 + k4 * vt2;
+    flux[0] = 0.5 * ((fl[0] + fr[0]) - diss_r);
+    flux[4] = 0.5 * ((fl[4] + fr[4]) - diss_E);
+    flux[mn] = 0.5 * ((fl[mn] + fr[mn]) - diss_n);
+    flux[mt1] = 0.5 * ((fl[mt1] + fr[mt1]) - diss_1);
+    flux[mt2] = 0.5 * ((fl[mt2] + fr[mt2]) - diss_2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Point decode + directional flux (physics.py:240-255, upwind.py:116-127)
+// ---------------------------------------------------------------------------
+template <int DIM, bool EXACT>
+__device__ __forceinline__ void point_flux(const double (&u)[NV], double gm1, double (&f)[NV],
+                                           double& rho_out, double& p_out) {
+  double vx, vy, vz, p;
+  if constexpr (EXACT) {
+    const double inv = xd(1.0, u[0]);
+    vx = xm(u[1], inv);
+    vy = xm(u[2], inv);
+    vz = xm(u[3], inv);
+    p = xm(gm1, xs(u[4], xm(xm(0.5, u[0]), xa(xa(xm(vx, vx), xm(vy, vy)), xm(vz, vz)))));
+  } else {
+    const double inv = frcp(u[0]);
+    vx = u[1] * inv;
+    vy = u[2] * inv;
+    vz = u[3] * inv;
+    p = gm1 * (u[4] - (0.5 * inv) * (u[1] * u[1] + u[2] * u[2] + u[3] * u[3]));
+  }
+  const double vd = DIM == 0 ? vx : (DIM == 1 ? vy : vz);
+  f[0] = u[1 + DIM];
+  if constexpr (EXACT) {
+    f[1] = xm(u[1], vd);
+    f[2] = xm(u[2], vd);
+    f[3] = xm(u[3], vd);
+    f[1 + DIM] = xa(f[1 + DIM], p);
+    f[4] = xm(xa(u[4], p), vd);
+  } else {
+    f[1] = u[1] * vd;
+    f[2] = u[2] * vd;
+    f[3] = u[3] * vd;
+    f[1 + DIM] += p;
+    f[4] = (u[4] + p) * vd;
+  }
+  rho_out = u[0];
+  p_out = p;
+}
+
+struct SweepArgs {
+  Geo geo;
+  Phys ph;
+  const double* u;
+  double* inc;
+  double inv_dx;
+  int seg;          // segment length
+  int accumulate;   // 0: inc = 0 - d ; 1: inc -= d
+  int check;        // latch positivity of interior points
+  unsigned long long* err;
+  int64_t tag;
+};
+
+// Line geometry: thread -> (line origin pointer offset, stride, transverse ok)
+template <int DIM>
+__device__ __forceinline__ bool line_of(const SweepArgs& a, int64_t& base, int& seg_id) {
+  const Geo& G = a.geo;
+  int i, j, k;
+  if (DIM == 0) {
+    j = blockIdx.x * blockDim.x + threadIdx.x;
+    k = blockIdx.y * blockDim.y + threadIdx.y;
+    if (j >= G.n[1] || k >= G.n[2]) return false;
+    i = 0;
+  } else if (DIM == 1) {
+    i = blockIdx.x * blockDim.x + threadIdx.x;
+    k = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= G.n[0] || k >= G.n[2]) return false;
+    j = 0;
+  } else {
+    i = blockIdx.x * blockDim.x + threadIdx.x;
+    j = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= G.n[0] || j >= G.n[1]) return false;
+    k = 0;
+  }
+  base = G.idx(i, j, k);
+  seg_id = blockIdx.z;
+  return true;
+}
+
+template <int DIM, bool EXACT>
+__global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
+  int64_t base;
+  int seg_id;
+  if (!line_of<DIM>(a, base, seg_id)) return;
+  const Geo& G = a.geo;
+  const int nd = G.n[DIM];
+  const int c0 = seg_id * a.seg;
+  if (c0 >= nd) return;
+  const int c1 = min(c0 + a.seg, nd);
+  const int64_t sd = G.stride(DIM);
+  const int64_t np = G.npts;
+  const double* __restrict__ u = a.u + base;
+  double* __restrict__ inc = a.inc + base;
+  const double gm1 = a.ph.gm1, eps = a.ph.eps;
+  const int power = a.ph.power;
+
+  // window: point w holds line position c - 2 + w (w = 0..4)
+  double wu[5][NV], wf[5][NV];
+
+  auto load = [&](int m, double (&uu)[NV], double (&ff)[NV]) {
+    const double* q = u + (int64_t)m * sd;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) uu[v] = __ldg(q + v * np);
+    double rho, p;
+    point_flux<DIM, EXACT>(uu, gm1, ff, rho, p);
+    if (a.check && m >= 0 && m < nd) {
+      if (!(rho > 0.0)) latch_error(a.err, a.tag, 1, base + (int64_t)m * sd);
+      else if (!(p > 0.0)) latch_error(a.err, a.tag, 2, base + (int64_t)m * sd);
+    }
+  };
+
+#pragma unroll
+  for (int w = 0; w < 4; ++w) load(c0 - 3 + w, wu[w + 1], wf[w + 1]);
+
+  double lu[NV], lf[NV];  // left states at c-1/2 (carried)
+  double fprev[NV];
+  for (int c = c0 - 1; c <= c1; ++c) {
+    // shift and load position c+2
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        wu[w][v] = wu[w + 1][v];
+        wf[w][v] = wf[w + 1][v];
+      }
+    }
+    load(c + 2, wu[4], wf[4]);
+    // reconstructions of window c: ru/rf at c-1/2, nu/nf at c+1/2
+    double ru[NV], rf[NV], nu[NV], nf[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
+    nf[0] = nu[1 + DIM];
+    rf[0] = ru[1 + DIM];
+#pragma unroll
+    for (int v = 1; v < NV; ++v)
+      recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
+    if (c >= c0) {
+      double flux[NV];
+      roe_flux<DIM, EXACT>(lu, ru, lf, rf, a.ph, flux);
+      if (c > c0) {
+        double* q = inc + (int64_t)(c - 1) * sd;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          if constexpr (EXACT) {
+            const double d = xm(xs(flux[v], fprev[v]), a.inv_dx);
+            q[v * np] = a.accumulate ? xs(q[v * np], d) : xs(0.0, d);
+          } else {
+            const double d = (flux[v] - fprev[v]) * a.inv_dx;
+            q[v * np] = a.accumulate ? q[v * np] - d : -d;
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) fprev[v] = flux[v];
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      lu[v] = nu[v];
+      lf[v] = nf[v];
+    }
+  }
+}
+
+template <int DIM, bool EXACT>
+static int launch_dim(const hd_plan* p, const SweepArgs& a, int nseg, cudaStream_t s) {
+  const Geo& G = p->geo;
+  dim3 block, grid;
+  if (DIM == 0) {
+    block = dim3(32, 4, 1);
+    grid = dim3((G.n[1] + 31) / 32, (G.n[2] + 3) / 4, nseg);
+  } else if (DIM == 1) {
+    block = dim3(32, 4, 1);
+    grid = dim3((G.n[0] + 31) / 32, (G.n[2] + 3) / 4, nseg);
+  } else {
+    block = dim3(32, 4, 1);
+    grid = dim3((G.n[0] + 31) / 32, (G.n[1] + 3) / 4, nseg);
+  }
+  sweep_kernel<DIM, EXACT><<<grid, block, 0, s>>>(a); hd::count_launches(1);
+  return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+}
+
+int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int accumulate, int check,
+                 int64_t tag, cudaStream_t s) {
+  if (dim < 0 || dim > 2) return HD_E_ARG;
+  const Geo& G = p->geo;
+  SweepArgs a;
+  a.geo = G;
+  a.ph = p->phys;
+  a.u = u;
+  a.inc = inc;
+  a.inv_dx = 1.0 / G.h[dim];
+  a.accumulate = accumulate;
+  a.check = check;
+  a.err = (unsigned long long*)(p->ws + p->off[HD_BUF_ERR]);
+  a.tag = tag;
+  // segment length: enough independent lines to fill ~6 waves of 148 SMs x 256 threads
+  const int64_t lines = (int64_t)G.n[0] * G.n[1] * G.n[2] / G.n[dim];
+  const int64_t target = (int64_t)p->sm_count * 256 * 6;
+  int nseg = (int)((target + lines - 1) / lines);
+  if (nseg < 1) nseg = 1;
+  if (nseg > G.n[dim] / 8) nseg = G.n[dim] / 8 > 0 ? G.n[dim] / 8 : 1;
+  a.seg = (G.n[dim] + nseg - 1) / nseg;
+  nseg = (G.n[dim] + a.seg - 1) / a.seg;
+  const bool exact = p->mode == HD_MODE_EXACT;
+  switch (dim * 2 + (exact ? 1 : 0)) {
+    case 0: return launch_dim<0, false>(p, a, nseg, s);
+    case 1: return launch_dim<0, true>(p, a, nseg, s);
+    case 2: return launch_dim<1, false>(p, a, nseg, s);
+    case 3: return launch_dim<1, true>(p, a, nseg, s);
+    case 4: return launch_dim<2, false>(p, a, nseg, s);
+    default: return launch_dim<2, true>(p, a, nseg, s);
+  }
+}
+
+}  // namespace hd

@@ -1,0 +1,238 @@
+"""CUDA path (libhd.so through the package API) against the oracle and the
+reference's golden vectors.
+
+Tolerances:
+* exact mode -- bitwise (np.array_equal) against vectors produced by the
+  reference itself: the kernels follow the reference operation order with
+  no FMA contraction;
+* fast mode -- the north-star bar, relative L2 <= 1e-10 per conserved
+  variable after N steps (BASELINE.json), and per-kernel max error
+  <= 1e-12 relative to the field scale.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rough_problem
+
+pytestmark = pytest.mark.gpu
+
+FAST_KERNEL_TOL = 1e-12
+TRAJ_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def hd():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2211_16718_b200 as hd
+
+    hd._lib.load(require_cuda=True)
+    return hd
+
+
+def _spec(hd, P):
+    return hd.GridSpec(P.n, P.length)
+
+
+def _fs(hd, P, flat):
+    return hd.FieldSet(_spec(hd, P), hd.Layout.COMPONENT_CONTIGUOUS, torch.from_numpy(flat.copy()).cuda())
+
+
+def _rel_l2(a, b):
+    a = a.reshape(5, -1)
+    b = b.reshape(5, -1)
+    return np.sqrt(np.sum((a - b) ** 2, axis=1)) / np.maximum(np.sqrt(np.sum(b ** 2, axis=1)), 1e-300)
+
+
+def _close(a, b, tol):
+    scale = max(np.max(np.abs(b)), 1e-300)
+    return np.max(np.abs(a - b)) <= tol * scale
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+@pytest.mark.parametrize("dim", [0, 1, 2])
+def test_hyper_sweep(hd, kernels_golden, mode, dim):
+    K = kernels_golden
+    P = rough_problem(K)
+    fs = _fs(hd, P, K["rough_u"])
+    inc = fs.like()
+    hd.hyper_sweep(fs, dim, inc, mode=mode)
+    got = inc.numpy()
+    want = K[f"sweep{dim}_inc"]
+    if mode == "exact":
+        assert np.array_equal(got, want)
+    else:
+        assert _close(got, want, FAST_KERNEL_TOL)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+@pytest.mark.parametrize("name,kw", [
+    ("hyper", {}),
+    ("hyper_delta", {"delta": 0.3}),
+    ("hyper_p3", {"params": "p3"}),
+])
+def test_hyperbolic_rhs(hd, kernels_golden, mode, name, kw):
+    K = kernels_golden
+    P = rough_problem(K)
+    fs = _fs(hd, P, K["rough_u"])
+    params = hd.WenoParams(epsilon=1e-5, power=3) if kw.get("params") == "p3" else hd.DEFAULT_PARAMS
+    out = hd.hyperbolic_rhs(fs, hd.GasModel(), params, kw.get("delta", 0.0), mode=mode).numpy()
+    if mode == "exact":
+        assert np.array_equal(out, K[name])
+    else:
+        assert _close(out, K[name], FAST_KERNEL_TOL)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_make_rhs(hd, kernels_golden, mode):
+    K = kernels_golden
+    P = rough_problem(K)
+    rhs = hd.make_rhs(hd.GasModel(mu=0.006), mode=mode)
+    for src, name in (("rough_u", "rhs"), ("rhs_unfilled_u", "rhs_unfilled")):
+        out = rhs(_fs(hd, P, K[src])).numpy()
+        if mode == "exact":
+            assert np.array_equal(out, K[name]), name
+        else:
+            assert _close(out, K[name], FAST_KERNEL_TOL), name
+
+
+@pytest.mark.parametrize("dim", [0, 1, 2])
+def test_central_derivative_4(hd, kernels_golden, dim):
+    K = kernels_golden
+    P = rough_problem(K)
+    e = torch.from_numpy(K["rough_u"].reshape((5,) + P.shape)[4].copy()).cuda()
+    out = hd.central_derivative_4(e, dim, P.length[dim] / P.n[dim], 3)
+    assert np.array_equal(out.cpu().numpy(), K[f"cd4_{dim}"])
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_rk4_trajectory16(hd, oracle, traj16_golden, mode):
+    T = traj16_golden
+    P = oracle.Problem(n=(16, 16, 16), mu=0.006)
+    fs = _fs(hd, P, oracle.from_interior(T["ic"], P))
+    res = hd.advance(fs, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=10),
+                     mode=mode)
+    got = res.fields.interior().cpu().numpy()
+    dts = np.array([r.dt for r in res.records])
+    if mode == "exact":
+        assert np.array_equal(dts, T["dt"])
+        assert np.array_equal(got, T["final"])
+        assert res.t == float(T["t"])
+    else:
+        assert np.max(np.abs(dts - T["dt"]) / T["dt"]) < 1e-12
+        assert np.all(_rel_l2(got, T["final"]) <= TRAJ_TOL)
+    mass = np.array([r.mass for r in res.records])
+    energy = np.array([r.energy for r in res.records])
+    assert np.allclose(mass, T["mass"], rtol=1e-13, atol=0)
+    assert np.allclose(energy, T["energy"], rtol=1e-13, atol=0)
+    assert np.allclose([r.max_wavespeed for r in res.records], T["max_wavespeed"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_rk3_trajectory16(hd, oracle, traj16_golden, mode):
+    T = traj16_golden
+    P = oracle.Problem(n=(16, 16, 16), mu=0.006)
+    fs = _fs(hd, P, oracle.from_interior(T["ic"], P))
+    res = hd.advance(fs, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk3", cfl=0.4, max_steps=3),
+                     mode=mode)
+    got = res.fields.interior().cpu().numpy()
+    if mode == "exact":
+        assert np.array_equal(got, T["rk3_final"])
+    else:
+        assert np.all(_rel_l2(got, T["rk3_final"]) <= TRAJ_TOL)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_config1_trajectory(hd, traj32_golden, mode):
+    """Config 1: 32^3 HIT IC, RK4, CFL 0.4, mu 0.006, 10 steps,
+    with the reference's kinetic-energy decay curve."""
+    G = traj32_golden
+    spec = hd.GridSpec((32, 32, 32))
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+    assert hashlib.sha256(ic.interior().cpu().numpy().tobytes()).hexdigest() == G["ic_sha256"]
+    res = hd.advance(ic, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=10),
+                     mode=mode)
+    fin = res.fields.interior().cpu().numpy()
+    l2 = np.sqrt(np.sum(fin.reshape(5, -1) ** 2, axis=1))
+    ke = [r.kinetic_energy for r in res.records]
+    if mode == "exact":
+        assert hashlib.sha256(fin.tobytes()).hexdigest() == G["final_sha256"]
+        assert [r.dt for r in res.records] == G["dt"]
+        assert res.t == G["t"]
+    assert np.all(np.abs(l2 - np.array(G["l2"])) / np.array(G["l2"]) <= TRAJ_TOL)
+    assert np.allclose(ke, G["ke"][1:], rtol=1e-11, atol=0)
+
+
+def test_fast_vs_exact_32(hd):
+    spec = hd.GridSpec((32, 32, 32))
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+    tp = hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=20)
+    a = hd.advance(ic, hd.GasModel(mu=0.006), tp, mode="exact").fields.interior().cpu().numpy()
+    b = hd.advance(ic, hd.GasModel(mu=0.006), tp, mode="fast").fields.interior().cpu().numpy()
+    assert np.all(_rel_l2(b, a) <= TRAJ_TOL)
+
+
+def test_step_error_reports_stage(hd):
+    """Negative energy -> StepError with step and stage (test_timeint.py:161-171)."""
+    spec = hd.GridSpec((8, 8, 8))
+    fs = hd.FieldSet.zeros(spec)
+    it = fs.interior()
+    it[0] = 1.0
+    it[4] = 2.5
+    it[4, 2, 3, 4] = -1.0
+    with pytest.raises(hd.InvalidStateError):
+        hd.advance(fs, hd.GasModel(), hd.TimeParams(scheme="rk4", dt=0.01, max_steps=2))
+    it[4, 2, 3, 4] = 2.5
+    it[1] = 0.01
+    # fixed dt, blow up in stage 1 of step 1: an absurd dt makes stage inputs negative
+    fs2 = hd.FieldSet.zeros(spec)
+    z = torch.linspace(0, 6.283, 8, dtype=torch.float64, device="cuda")
+    fs2.interior()[0] = 1.0 + 0.5 * torch.sin(z)[None, None, :]
+    fs2.interior()[4] = 2.5
+    with pytest.raises(hd.StepError) as ei:
+        hd.advance(fs2, hd.GasModel(), hd.TimeParams(scheme="rk4", dt=50.0, max_steps=3))
+    assert ei.value.step == 1 and ei.value.stage in (1, 2, 3)
+
+
+def test_uniform_flow_zero_rhs(hd):
+    n = 12
+    spec = hd.GridSpec((n, n, n))
+    fs = hd.FieldSet.zeros(spec)
+    it = fs.interior()
+    rho, u, p = 1.1, 0.4, 0.9
+    it[0] = rho
+    it[1] = rho * u
+    it[2] = rho * 0.2 * u
+    it[3] = -rho * 0.1 * u
+    it[4] = p / 0.4 + 0.5 * rho * (u * u * (1 + 0.04 + 0.01))
+    hd.fill_ghosts_periodic(fs)
+    for mode in ("exact", "fast"):
+        out = hd.hyperbolic_rhs(fs, hd.GasModel(), mode=mode)
+        assert out.interior().abs().max().item() < 1e-13
+
+
+def test_fixed_dt_lands_on_t_final(hd):
+    spec = hd.GridSpec((16, 16, 16))
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+    seen = []
+    res = hd.advance(ic, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", dt=0.03, t_final=0.1),
+                     observer=seen.append)
+    assert res.steps == 4 and len(seen) == 4
+    assert abs(res.t - 0.1) < 1e-15
+    assert abs(res.records[-1].dt - (0.1 - 0.09)) < 1e-15
+
+
+def test_inviscid_conservation(hd):
+    """Acceptance analogue (test_acceptance.py:315-341) on 32^3, 40 RK4 steps."""
+    spec = hd.GridSpec((32, 32, 32))
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+    m0, mom0, e0 = hd.conserved_totals(ic)
+    res = hd.advance(ic, hd.GasModel(), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=40))
+    m1, mom1, e1 = hd.conserved_totals(res.fields)
+    assert abs(m1 - m0) / abs(m0) < 1e-11
+    assert abs(e1 - e0) / abs(e0) < 1e-11
+    assert max(abs(a - b) for a, b in zip(mom0, mom1)) < 1e-11
