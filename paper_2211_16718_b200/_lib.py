@@ -13,7 +13,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhd.so")
+LIB_PATH = os.environ.get("HD_LIB") or os.path.join(HERE, "libhd.so")
 CSRC = os.path.join(HERE, "csrc")
 
 HD_OK = 0

@@ -280,6 +280,12 @@ __device__ __forceinline__ void point_flux(const double (&u)[NV], double gm1, do
   p_out = p;
 }
 
+constexpr int SWEEP_THREADS = 64;
+#ifndef HD_SWEEP_MIN_BLOCKS
+#define HD_SWEEP_MIN_BLOCKS 4
+#endif
+constexpr int SWEEP_MIN_BLOCKS = HD_SWEEP_MIN_BLOCKS;  // blocks of 64 threads per SM (register cap)
+
 struct SweepArgs {
   Geo geo;
   Phys ph;
@@ -320,7 +326,7 @@ __device__ __forceinline__ bool line_of(const SweepArgs& a, int64_t& base, int& 
 }
 
 template <int DIM, bool EXACT>
-__global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(const SweepArgs a) {
   int64_t base;
   int seg_id;
   if (!line_of<DIM>(a, base, seg_id)) return;
@@ -339,10 +345,17 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
   // window: point w holds line position c - 2 + w (w = 0..4)
   double wu[5][NV], wf[5][NV];
 
-  auto load = [&](int m, double (&uu)[NV], double (&ff)[NV]) {
+  // raw loads are issued one iteration before the point enters the window
+  // (and the inc read of a cell at the top of the iteration that writes it),
+  // so HBM/L2 latency hides behind a full window of FP64 work
+  auto fetch = [&](int m, double (&dst)[NV]) {
     const double* q = u + (int64_t)m * sd;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) uu[v] = __ldg(q + v * np);
+    for (int v = 0; v < NV; ++v) dst[v] = __ldg(q + v * np);
+  };
+  auto ingest = [&](int m, const double (&src)[NV], double (&uu)[NV], double (&ff)[NV]) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) uu[v] = src[v];
     double rho, p;
     point_flux<DIM, EXACT>(uu, gm1, ff, rho, p);
     if (a.check && m >= 0 && m < nd) {
@@ -351,13 +364,18 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     }
   };
 
+  double pre[NV];
 #pragma unroll
-  for (int w = 0; w < 4; ++w) load(c0 - 3 + w, wu[w + 1], wf[w + 1]);
+  for (int w = 0; w < 4; ++w) {
+    fetch(c0 - 3 + w, pre);
+    ingest(c0 - 3 + w, pre, wu[w + 1], wf[w + 1]);
+  }
+  fetch(c0 + 1, pre);
 
   double lu[NV], lf[NV];  // left states at c-1/2 (carried)
   double fprev[NV];
   for (int c = c0 - 1; c <= c1; ++c) {
-    // shift and load position c+2
+    // shift; position c+2 enters from the prefetch buffer
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
 #pragma unroll
@@ -366,7 +384,13 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
         wf[w][v] = wf[w + 1][v];
       }
     }
-    load(c + 2, wu[4], wf[4]);
+    ingest(c + 2, pre, wu[4], wf[4]);
+    if (c < c1) fetch(c + 3, pre);
+    const bool wr = c > c0;
+    double* q = inc + (int64_t)(c - 1) * sd;
+    double old[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) old[v] = (wr && a.accumulate) ? q[v * np] : 0.0;
     // reconstructions of window c: ru/rf at c-1/2, nu/nf at c+1/2
     double ru[NV], rf[NV], nu[NV], nf[NV];
 #pragma unroll
@@ -380,16 +404,14 @@ __global__ void __launch_bounds__(128) sweep_kernel(const SweepArgs a) {
     if (c >= c0) {
       double flux[NV];
       roe_flux<DIM, EXACT>(lu, ru, lf, rf, a.ph, flux);
-      if (c > c0) {
-        double* q = inc + (int64_t)(c - 1) * sd;
+      if (wr) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
+          // accumulate: inc -= d ; first sweep of an RHS: inc = 0 - d (upwind.py:181-182)
           if constexpr (EXACT) {
-            const double d = xm(xs(flux[v], fprev[v]), a.inv_dx);
-            q[v * np] = a.accumulate ? xs(q[v * np], d) : xs(0.0, d);
+            q[v * np] = xs(old[v], xm(xs(flux[v], fprev[v]), a.inv_dx));
           } else {
-            const double d = (flux[v] - fprev[v]) * a.inv_dx;
-            q[v * np] = a.accumulate ? q[v * np] - d : -d;
+            q[v * np] = old[v] - (flux[v] - fprev[v]) * a.inv_dx;
           }
         }
       }
@@ -408,16 +430,11 @@ template <int DIM, bool EXACT>
 static int launch_dim(const hd_plan* p, const SweepArgs& a, int nseg, cudaStream_t s) {
   const Geo& G = p->geo;
   dim3 block, grid;
-  if (DIM == 0) {
-    block = dim3(32, 4, 1);
-    grid = dim3((G.n[1] + 31) / 32, (G.n[2] + 3) / 4, nseg);
-  } else if (DIM == 1) {
-    block = dim3(32, 4, 1);
-    grid = dim3((G.n[0] + 31) / 32, (G.n[2] + 3) / 4, nseg);
-  } else {
-    block = dim3(32, 4, 1);
-    grid = dim3((G.n[0] + 31) / 32, (G.n[1] + 3) / 4, nseg);
-  }
+  constexpr int BY = SWEEP_THREADS / 32;
+  block = dim3(32, BY, 1);
+  if (DIM == 0) grid = dim3((G.n[1] + 31) / 32, (G.n[2] + BY - 1) / BY, nseg);
+  else if (DIM == 1) grid = dim3((G.n[0] + 31) / 32, (G.n[2] + BY - 1) / BY, nseg);
+  else grid = dim3((G.n[0] + 31) / 32, (G.n[1] + BY - 1) / BY, nseg);
   sweep_kernel<DIM, EXACT><<<grid, block, 0, s>>>(a); hd::count_launches(1);
   return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
 }

@@ -111,7 +111,7 @@ def _synth_torch(n: int, params: HitParams, device):
     vel = []
     c = torch.complex(torch.randn((3, n, n, n), generator=gen, dtype=torch.float64, device=device),
                       torch.randn((3, n, n, n), generator=gen, dtype=torch.float64, device=device))
-    c = 0.5 * (c + torch.conj(torch.roll(torch.flip(c, dims=(1, 2, 3)), 1, dims=(1, 2, 3))))
+    c = 0.5 * (c + torch.conj(torch.roll(torch.flip(c, dims=(1, 2, 3)), (1, 1, 1), dims=(1, 2, 3))))
     c *= ((shell >= 1) & (shell < n // 2)).to(torch.float64)
     k2 = kx * kx + ky * ky + kz * kz
     kdot = (kx * c[0] + ky * c[1] + kz * c[2]) / torch.where(k2 == 0.0, torch.ones_like(k2), k2)

@@ -184,18 +184,25 @@ def test_step_error_reports_stage(hd):
     it[0] = 1.0
     it[4] = 2.5
     it[4, 2, 3, 4] = -1.0
-    with pytest.raises(hd.InvalidStateError):
+    # CFL sizing decodes the state first: compute_dt raises InvalidStateError (timeint.py:235)
+    with pytest.raises(hd.InvalidStateError) as ei:
+        hd.advance(fs, hd.GasModel(), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=2))
+    assert not isinstance(ei.value, hd.StepError)
+    # fixed dt: the first RHS decode fails -> StepError(step 1, stage 0) (timeint.py:161-165, 238-241)
+    with pytest.raises(hd.StepError) as ei:
         hd.advance(fs, hd.GasModel(), hd.TimeParams(scheme="rk4", dt=0.01, max_steps=2))
-    it[4, 2, 3, 4] = 2.5
-    it[1] = 0.01
-    # fixed dt, blow up in stage 1 of step 1: an absurd dt makes stage inputs negative
+    assert ei.value.step == 1 and ei.value.stage == 0
+    # a valid state with an absurd fixed dt: the stage-1 input u + (dt/2) k1 has
+    # negative density, so the second RHS evaluation fails -> StepError(step 1, stage 1)
     fs2 = hd.FieldSet.zeros(spec)
-    z = torch.linspace(0, 6.283, 8, dtype=torch.float64, device="cuda")
-    fs2.interior()[0] = 1.0 + 0.5 * torch.sin(z)[None, None, :]
-    fs2.interior()[4] = 2.5
+    x = torch.arange(8, dtype=torch.float64, device="cuda") * (2 * np.pi / 8)
+    w = 0.9 * torch.sin(x)[:, None, None]  # z velocity varying along z
+    fs2.interior()[0] = 1.0
+    fs2.interior()[3] = w
+    fs2.interior()[4] = 2.5 + 0.5 * w * w
     with pytest.raises(hd.StepError) as ei:
         hd.advance(fs2, hd.GasModel(), hd.TimeParams(scheme="rk4", dt=50.0, max_steps=3))
-    assert ei.value.step == 1 and ei.value.stage in (1, 2, 3)
+    assert ei.value.step == 1 and ei.value.stage == 1
 
 
 def test_uniform_flow_zero_rhs(hd):
