@@ -43,19 +43,21 @@ extern "C" {
 #define HD_SCHEME_RK3 3
 #define HD_SCHEME_RK4 4
 
-/* stage parts for decomposed runs (hd_stage_part) */
-#define HD_PART_LOCAL 1   /* sweeps along locally-periodic axes */
-#define HD_PART_HALO 2    /* sweeps along exchanged axes + viscous fluxes */
-#define HD_PART_DIVLOC 4  /* viscous divergence along locally-periodic axes */
-#define HD_PART_UPDATE 8  /* divergence along exchanged axes + RK stage update */
+/* stage parts (hd_stage_part): one RK stage, split around the halo seam.
+ * Call in order; between LOCAL and HALO the z ghosts of the stage input must
+ * arrive, between HALO and DIV the z ghosts of the viscous z-flux group. */
+#define HD_PART_LOCAL 1   /* x, y sweeps (fast: + viscous primitives): no z ghosts read */
+#define HD_PART_HALO 2    /* exact: z sweep + primitives; both: viscous fluxes */
+#define HD_PART_DIV 4     /* fast: viscous divergence added to the increment */
+#define HD_PART_UPDATE 8  /* fast: z sweep + RK update; exact: divergence + RK update */
 #define HD_PART_ALL 15
 
 /* workspace buffers (hd_plan_buffer) */
-#define HD_BUF_STAGE 0 /* 5 fields: RK stage state */
+#define HD_BUF_STAGE 0 /* 10 fields: RK stage states, ping-pong halves (stage s writes half s%2) */
 #define HD_BUF_ACC 1   /* 5 fields: RK4 accumulator */
 #define HD_BUF_INC 2   /* 5 fields: RHS increment */
 #define HD_BUF_PRIM 3  /* 4 fields: u, v, w, T */
-#define HD_BUF_VFLUX 4 /* 12 fields: viscous flux F_d[r], d-major */
+#define HD_BUF_VFLUX 4 /* 9 fields: symmetric viscous fluxes tau00 tau01 tau11 w0 w1 | tau02 tau12 tau22 w2 */
 #define HD_BUF_RED 5   /* reduction partials + results */
 #define HD_BUF_CTX 6   /* step context: t, dt, ... */
 #define HD_BUF_ERR 7   /* error key (uint64) */
@@ -147,8 +149,8 @@ int hd_step(hd_plan* plan, int scheme, double* u, const double* dt_dev, int64_t 
             void* stream);
 
 /* One part of one RK stage (decomposed runs).  Stage s reads u (s == 0) or
- * the workspace STAGE buffer; the UPDATE part writes the next stage state
- * (or u itself after the last stage). */
+ * half (s-1)%2 of the workspace STAGE buffer; the UPDATE part writes the next
+ * stage state into half s%2 (or u itself after the last stage). */
 int hd_stage_part(hd_plan* plan, int scheme, int stage, int parts, double* u,
                   const double* dt_dev, int64_t tag, void* stream);
 

@@ -21,7 +21,7 @@ HD_MODE_FAST = 0
 HD_MODE_EXACT = 1
 HD_SCHEME_RK3 = 3
 HD_SCHEME_RK4 = 4
-HD_PART_LOCAL, HD_PART_HALO, HD_PART_DIVLOC, HD_PART_UPDATE, HD_PART_ALL = 1, 2, 4, 8, 15
+HD_PART_LOCAL, HD_PART_HALO, HD_PART_DIV, HD_PART_UPDATE, HD_PART_ALL = 1, 2, 4, 8, 15
 (HD_BUF_STAGE, HD_BUF_ACC, HD_BUF_INC, HD_BUF_PRIM, HD_BUF_VFLUX, HD_BUF_RED, HD_BUF_CTX,
  HD_BUF_ERR) = range(8)
 (HD_RED_SIGNAL_MAX, HD_RED_SIGNAL_SUM, HD_RED_WAVESPEED, HD_RED_MASS, HD_RED_MOMX, HD_RED_MOMY,

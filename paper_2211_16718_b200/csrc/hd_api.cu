@@ -46,7 +46,7 @@ int64_t npts_of(const hd_geom* g) {
 void layout(const hd_geom* g, int64_t off[HD_NBUF], int64_t* total) {
   const int64_t f = npts_of(g) * 8;
   int64_t o = 0;
-  const int64_t sizes[HD_NBUF] = {5 * f, 5 * f, 5 * f, 4 * f, 12 * f, RED_BYTES, 8 * HD_CTX_N, 64};
+  const int64_t sizes[HD_NBUF] = {10 * f, 5 * f, 5 * f, 4 * f, 9 * f, RED_BYTES, 8 * HD_CTX_N, 64};
   for (int b = 0; b < HD_NBUF; ++b) {
     off[b] = o;
     o = align_up(o + sizes[b]);
@@ -67,12 +67,6 @@ bool parts_supported(const hd_plan* p) {
   return true;
 }
 
-int mask_of(const hd_plan* p, bool periodic) {
-  int m = 0;
-  for (int d = 0; d < 3; ++d)
-    if ((p->geo.periodic[d] != 0) == periodic) m |= 1 << d;
-  return m;
-}
 
 // sweeps for the dims in `dmask`, in x, y, z order; the first sweep of the
 // RHS overwrites inc (0 - d, upwind.py:181-182) unless `accumulate_first`.
@@ -89,6 +83,11 @@ int sweeps(hd_plan* p, int dmask, const double* us, double* inc, bool first_over
 }
 
 int nstages(int scheme) { return scheme == HD_SCHEME_RK3 ? 3 : 4; }
+
+// stage s > 0 reads the ping-pong half (s-1)%2 of the STAGE buffer (see make_rk)
+const double* stage_input(hd_plan* p, int stage, const double* u) {
+  return stage == 0 ? u : buf(p, HD_BUF_STAGE) + ((stage - 1) % 2) * NV * p->geo.npts;
+}
 
 }  // namespace
 
@@ -226,27 +225,46 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   if (!p || !u || (scheme != HD_SCHEME_RK3 && scheme != HD_SCHEME_RK4)) return HD_E_ARG;
   if (!p->ws) return HD_E_WORKSPACE;
   if (stage < 0 || stage >= nstages(scheme)) return HD_E_ARG;
-  if (!parts_supported(p)) return HD_E_UNSUPPORTED;
+  // the fused pipeline decomposes along z only (x and y wrap locally)
+  if (!p->geo.periodic[0] || !p->geo.periodic[1]) return HD_E_UNSUPPORTED;
   cudaStream_t s = S(stream);
-  const double* us = stage == 0 ? u : buf(p, HD_BUF_STAGE);
+  const double* us = stage_input(p, stage, u);
   double* inc = buf(p, HD_BUF_INC);
-  const int loc = mask_of(p, true), ex = mask_of(p, false);
   const bool visc = p->phys.mu != 0.0;
   const int64_t t = tag * 8 + 1 + stage;  // slot 1..4: RK stage (0 = pre-step CFL, 7 = diagnostics)
   int rc = HD_OK;
-  if ((parts & HD_PART_LOCAL) && loc) rc = sweeps(p, loc, us, inc, true, t, s);
+  const bool exact = p->mode == HD_MODE_EXACT;
+  double* prim = visc ? buf(p, HD_BUF_PRIM) : nullptr;
+  // LOCAL: x and y sweeps (fast: the y sweep also stores the viscous primitives).
+  // Neither reads z ghosts, so a z-halo exchange of `us` can be in flight.
+  if (parts & HD_PART_LOCAL) {
+    rc = launch_sweep(p, 0, us, inc, 0, 1, t, s);
+    if (!rc) rc = exact ? launch_sweep(p, 1, us, inc, 1, 0, t, s)
+                        : launch_sweep_prims(p, us, inc, prim, t, s);
+  }
+  // HALO (reads the z ghosts of `us`)
+  //   exact: z sweep, primitives of the whole box, viscous fluxes
+  //   fast:  primitives of exchanged ghost planes, viscous fluxes
   if (!rc && (parts & HD_PART_HALO)) {
-    if (ex) rc = sweeps(p, ex, us, inc, loc == 0, t, s);
-    if (!rc && visc) rc = launch_prims(p, us, s);
+    if (exact) {
+      rc = launch_sweep(p, 2, us, inc, 1, 0, t, s);
+      if (!rc && visc) rc = launch_prims(p, us, s);
+    } else if (visc && !p->geo.periodic[2]) {
+      const int g = p->geo.g, nz = p->geo.n[2];
+      rc = launch_prims_planes(p, us, 0, g, s);
+      if (!rc) rc = launch_prims_planes(p, us, nz + g, nz + 2 * g, s);
+    }
     if (!rc && visc) rc = launch_gradflux(p, s);
   }
-  if (!rc && (parts & HD_PART_DIVLOC) && visc && ex && loc)
-    rc = launch_divergence(p, loc, inc, inc, 0, scheme, stage, nullptr, nullptr, s);
+  // DIV (reads the z ghosts of the viscous z-flux group) -- fast: inc += div F
+  if (!rc && (parts & HD_PART_DIV) && !exact && visc)
+    rc = launch_divergence(p, 7, inc, inc, 0, scheme, stage, nullptr, nullptr, s);
+  // UPDATE: RK stage update (exact: after the viscous divergence, viscous.py:112-120
+  // order; fast: fused into the z sweep, the divergence having been added by DIV)
   if (!rc && (parts & HD_PART_UPDATE)) {
     if (!dt_dev) return HD_E_ARG;
-    // with no exchanged axis the whole divergence happens here (single fused pass)
-    const int dmask = visc ? (ex ? ex : 7) : 0;
-    rc = launch_divergence(p, dmask, inc, nullptr, 1, scheme, stage, u, dt_dev, s);
+    rc = exact ? launch_divergence(p, visc ? 7 : 0, inc, nullptr, 1, scheme, stage, u, dt_dev, s)
+               : launch_sweep_update(p, us, inc, scheme, stage, u, dt_dev, t, s);
   }
   return rc;
 }

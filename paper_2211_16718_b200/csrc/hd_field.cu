@@ -2,14 +2,14 @@
 //
 //   fill_ghosts_kernel   grid.py:211-251   (_wrap_axis x -> y -> z, full extents)
 //   prims_kernel         physics.py:240-255 + viscous.py:80-81 (u, v, w, T = gamma p / rho)
-//   gradflux_kernel      viscous.py:86-116 (12 central gradients -> tau, q -> 12 flux fields,
+//   gradflux_kernel      viscous.py:86-116 (12 central gradients -> tau, q -> 9 flux fields,
 //                        periodic images along the flux's own axis = the sync_scalars it needs)
 //   divergence_kernel    viscous.py:119-120 (inc[1..4] += D_d F_d, d = 0, 1, 2), fused with
 //                        the RK stage update timeint.py:168-193
 //   rk_update_kernel     timeint.py:168-193 when mu == 0 (viscous.py:72-73 short-circuit)
 //   central_diff4_kernel kernels.py:207-227 (stand-alone, for the operator API)
 //   reduce kernels       timeint.py:100-131 (CFL signal, totals, max wavespeed, KE)
-#include "hd_internal.cuh"
+#include "hd_device.cuh"
 
 namespace hd {
 
@@ -69,9 +69,9 @@ int launch_fill_ghosts(const hd_plan* p, double* f, int nfields, int axis_mask, 
 // ---------------------------------------------------------------------------
 template <bool EXACT>
 __global__ void prims_kernel(const double* __restrict__ u, double* __restrict__ prim, Geo G,
-                             Phys ph) {
+                             Phys ph, int64_t q_lo, int64_t q_hi) {
   const int64_t np = G.npts;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < np;
+  for (int64_t q = q_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < q_hi;
        q += (int64_t)gridDim.x * blockDim.x) {
     const double rho = __ldg(u + q), m1 = __ldg(u + np + q), m2 = __ldg(u + 2 * np + q),
                  m3 = __ldg(u + 3 * np + q), E = __ldg(u + 4 * np + q);
@@ -98,57 +98,33 @@ __global__ void prims_kernel(const double* __restrict__ u, double* __restrict__ 
   }
 }
 
-int launch_prims(const hd_plan* p, const double* u, cudaStream_t s) {
+static int prims_range(const hd_plan* p, const double* u, int64_t q_lo, int64_t q_hi,
+                       cudaStream_t s) {
+  if (q_hi <= q_lo) return HD_OK;
   double* prim = (double*)(p->ws + p->off[HD_BUF_PRIM]);
-  int blocks = p->sm_count * 8;
+  int64_t want = (q_hi - q_lo + 255) / 256;
+  int blocks = (int)(want < p->sm_count * 8 ? want : p->sm_count * 8);
   if (p->mode == HD_MODE_EXACT)
-    prims_kernel<true><<<blocks, 256, 0, s>>>(u, prim, p->geo, p->phys);
+    prims_kernel<true><<<blocks, 256, 0, s>>>(u, prim, p->geo, p->phys, q_lo, q_hi);
   else
-    prims_kernel<false><<<blocks, 256, 0, s>>>(u, prim, p->geo, p->phys);
+    prims_kernel<false><<<blocks, 256, 0, s>>>(u, prim, p->geo, p->phys, q_lo, q_hi);
   hd::count_launches(1);
   return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
 }
 
-// ((-s[+2] + 8 s[+1]) - 8 s[-1]) + s[-2], times coef (kernels.py:221-226)
-template <bool EXACT>
-__device__ __forceinline__ double cd4(const double* __restrict__ s, int64_t st, double coef) {
-  const double p2 = __ldg(s + 2 * st), p1 = __ldg(s + st), m1 = __ldg(s - st),
-               m2 = __ldg(s - 2 * st);
-  if constexpr (EXACT) return xm(xa(xs(xa(-p2, xm(8.0, p1)), xm(8.0, m1)), m2), coef);
-  return (8.0 * (p1 - m1) + (m2 - p2)) * coef;
+int launch_prims(const hd_plan* p, const double* u, cudaStream_t s) {
+  return prims_range(p, u, 0, p->geo.npts, s);
 }
 
-// Writes v at interior point (i,j,k) of field f and at its periodic images
-// along the axes in `mask` (only those that wrap locally).
-__device__ __forceinline__ void store_with_images(double* f, const Geo& G, int i, int j, int k,
-                                                  int mask, double v) {
-  int ox[3], oy[3], oz[3];
-  int nx = 1, ny = 1, nz = 1;
-  ox[0] = 0; oy[0] = 0; oz[0] = 0;
-  const int g = G.g;
-  if (mask & 1) {
-    if (i + G.n[0] < G.n[0] + g) ox[nx++] = G.n[0];
-    if (i - G.n[0] >= -g) ox[nx++] = -G.n[0];
-  }
-  if (mask & 2) {
-    if (j + G.n[1] < G.n[1] + g) oy[ny++] = G.n[1];
-    if (j - G.n[1] >= -g) oy[ny++] = -G.n[1];
-  }
-  if (mask & 4) {
-    if (k + G.n[2] < G.n[2] + g) oz[nz++] = G.n[2];
-    if (k - G.n[2] >= -g) oz[nz++] = -G.n[2];
-  }
-  for (int c = 0; c < nz; ++c)
-    for (int b = 0; b < ny; ++b)
-      for (int a = 0; a < nx; ++a) f[G.idx(i + ox[a], j + oy[b], k + oz[c])] = v;
+// ghosted z planes [z_lo, z_hi), full x-y extent (decomposed runs: exchanged ghosts)
+int launch_prims_planes(const hd_plan* p, const double* u, int z_lo, int z_hi, cudaStream_t s) {
+  return prims_range(p, u, (int64_t)z_lo * p->geo.sz, (int64_t)z_hi * p->geo.sz, s);
 }
 
-__device__ __forceinline__ int periodic_mask(const Geo& G) {
-  return (G.periodic[0] ? 1 : 0) | (G.periodic[1] ? 2 : 0) | (G.periodic[2] ? 4 : 0);
-}
 
 // ---------------------------------------------------------------------------
-// viscous fluxes: 12 gradients -> tau, heat flux -> F_d = (tau_0d, tau_1d, tau_2d, work_d)
+// viscous fluxes: 12 gradients -> tau, heat flux -> F_d = (tau_0d, tau_1d, tau_2d, work_d),
+// stored symmetrically as 9 fields (hd_device.cuh VF_*)
 // ---------------------------------------------------------------------------
 template <bool EXACT>
 __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict__ prim,
@@ -190,23 +166,22 @@ __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict_
     tau[0][2] = tau[2][0] = mu * (gr[0][2] + gr[2][0]);
     tau[1][2] = tau[2][1] = mu * (gr[1][2] + gr[2][1]);
   }
-  const int pm = periodic_mask(G);
+  double w[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    double work;
     if constexpr (EXACT) {
       const double qd = xm(q_coef, gT[d]);
-      work = xs(xa(xa(xm(vel[0], tau[0][d]), xm(vel[1], tau[1][d])), xm(vel[2], tau[2][d])), qd);
+      w[d] = xs(xa(xa(xm(vel[0], tau[0][d]), xm(vel[1], tau[1][d])), xm(vel[2], tau[2][d])), qd);
     } else {
-      work = vel[0] * tau[0][d] + vel[1] * tau[1][d] + vel[2] * tau[2][d] - q_coef * gT[d];
+      w[d] = vel[0] * tau[0][d] + vel[1] * tau[1][d] + vel[2] * tau[2][d] - q_coef * gT[d];
     }
-    double* F = vf + (int64_t)(4 * d) * np;
-    const int m = pm & (1 << d);  // images along the flux's own axis only
-    store_with_images(F, G, i, j, k, m, tau[0][d]);
-    store_with_images(F + np, G, i, j, k, m, tau[1][d]);
-    store_with_images(F + 2 * np, G, i, j, k, m, tau[2][d]);
-    store_with_images(F + 3 * np, G, i, j, k, m, work);
   }
+  const double val[VF_N] = {tau[0][0], tau[0][1], tau[1][1], w[0], w[1],
+                            tau[0][2], tau[1][2], tau[2][2], w[2]};
+  const int pm = periodic_mask(G);
+#pragma unroll
+  for (int f = 0; f < VF_N; ++f)
+    store_face_images(vf + (int64_t)f * np, G, i, j, k, pm & vf_axes(f), val[f]);
 }
 
 int launch_gradflux(const hd_plan* p, cudaStream_t s) {
@@ -224,72 +199,6 @@ int launch_gradflux(const hd_plan* p, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
 }
 
-// ---------------------------------------------------------------------------
-// RK stage update (timeint.py:168-193), per point and variable
-// ---------------------------------------------------------------------------
-struct RKArgs {
-  int scheme, stage;
-  double* u;         // step base state (in/out for the last stage)
-  double* stage_buf; // stage state buffer (in: stage input for RK3 s>0; out: next stage)
-  double* acc;       // RK4 accumulator
-  const double* dt;  // device dt
-};
-
-template <bool EXACT>
-__device__ __forceinline__ void rk_point(const RKArgs& r, double dt, int64_t off, double k,
-                                         double& out, bool& to_u) {
-  const double u0 = r.u[off];
-  if (r.scheme == HD_SCHEME_RK4) {
-    if constexpr (EXACT) {
-      const double half = xm(0.5, dt);
-      switch (r.stage) {
-        case 0: r.acc[off] = k; out = xa(u0, xm(half, k)); to_u = false; break;
-        case 1: r.acc[off] = xa(r.acc[off], xm(2.0, k)); out = xa(u0, xm(half, k)); to_u = false; break;
-        case 2: r.acc[off] = xa(r.acc[off], xm(2.0, k)); out = xa(u0, xm(dt, k)); to_u = false; break;
-        default: out = xa(u0, xm(xd(dt, 6.0), xa(r.acc[off], k))); to_u = true; break;
-      }
-    } else {
-      const double half = 0.5 * dt;
-      switch (r.stage) {
-        case 0: r.acc[off] = k; out = u0 + half * k; to_u = false; break;
-        case 1: r.acc[off] = r.acc[off] + 2.0 * k; out = u0 + half * k; to_u = false; break;
-        case 2: r.acc[off] = r.acc[off] + 2.0 * k; out = u0 + dt * k; to_u = false; break;
-        default: out = u0 + (dt * (1.0 / 6.0)) * (r.acc[off] + k); to_u = true; break;
-      }
-    }
-  } else {  // TVD-RK3
-    if constexpr (EXACT) {
-      switch (r.stage) {
-        case 0: out = xa(u0, xm(dt, k)); to_u = false; break;
-        case 1: out = xa(xm(0.75, u0), xm(0.25, xa(r.stage_buf[off], xm(dt, k)))); to_u = false; break;
-        default:
-          out = xa(xm(1.0 / 3.0, u0), xm(2.0 / 3.0, xa(r.stage_buf[off], xm(dt, k)))); to_u = true; break;
-      }
-    } else {
-      switch (r.stage) {
-        case 0: out = u0 + dt * k; to_u = false; break;
-        case 1: out = 0.75 * u0 + 0.25 * (r.stage_buf[off] + dt * k); to_u = false; break;
-        default: out = (1.0 / 3.0) * u0 + (2.0 / 3.0) * (r.stage_buf[off] + dt * k); to_u = true; break;
-      }
-    }
-  }
-}
-
-template <bool EXACT>
-__device__ __forceinline__ void rk_store(const RKArgs& r, const Geo& G, int i, int j, int k,
-                                         const double (&kv)[NV]) {
-  const double dt = *r.dt;
-  const int64_t q = G.idx(i, j, k);
-  const int pm = periodic_mask(G);
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double out;
-    bool to_u;
-    rk_point<EXACT>(r, dt, q + v * G.npts, kv[v], out, to_u);
-    store_with_images((to_u ? r.u : r.stage_buf) + v * G.npts, G, i, j, k, pm, out);
-  }
-}
-
 // inc_out[r] = ((inc_in[r] + D0 F0[r]) + D1 F1[r]) + D2 F2[r] for the d's in dmask;
 // then either store, or apply the RK stage update.
 template <bool EXACT>
@@ -302,21 +211,10 @@ __global__ void __launch_bounds__(128) divergence_kernel(const double* __restric
   if (i >= G.n[0] || j >= G.n[1]) return;
   const int64_t np = G.npts;
   const int64_t q = G.idx(i, j, k);
-  const int64_t st[3] = {1, G.sy, G.sz};
   double kv[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) kv[v] = inc_in[q + v * np];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    if (!(dmask & (1 << d))) continue;
-    const double coef = 1.0 / (12.0 * G.h[d]);
-#pragma unroll
-    for (int row = 1; row < NV; ++row) {
-      const double dv = cd4<EXACT>(vf + (int64_t)(4 * d + row - 1) * np + q, st[d], coef);
-      if constexpr (EXACT) kv[row] = xa(kv[row], dv);
-      else kv[row] += dv;
-    }
-  }
+  add_viscous_divergence<EXACT>(vf, G, q, dmask, kv);
   if (update) {
     rk_store<EXACT>(r, G, i, j, k, kv);
   } else {
@@ -325,14 +223,37 @@ __global__ void __launch_bounds__(128) divergence_kernel(const double* __restric
   }
 }
 
-static RKArgs make_rk(const hd_plan* p, int scheme, int stage, double* u, const double* dt_dev) {
+RKArgs make_rk(const hd_plan* p, int scheme, int stage, double* u, const double* dt_dev) {
   RKArgs r;
   r.scheme = scheme;
   r.stage = stage;
   r.u = u;
-  r.stage_buf = (double*)(p->ws + p->off[HD_BUF_STAGE]);
+  // stage states ping-pong between the two halves of the STAGE buffer so a
+  // fused sweep never overwrites points other threads still read:
+  // stage s reads half (s-1)%2 (u for s = 0) and writes half s%2
+  double* st = (double*)(p->ws + p->off[HD_BUF_STAGE]);
+  const int64_t nf = NV * p->geo.npts;
+  r.stage_in = stage == 0 ? u : st + ((stage - 1) % 2) * nf;
+  r.stage_out = st + (stage % 2) * nf;
   r.acc = (double*)(p->ws + p->off[HD_BUF_ACC]);
   r.dt = dt_dev;
+  // fast-mode coefficients of the same tableaux (timeint.py:168-193)
+  r.a0 = 1.0; r.a1 = 0.0; r.kc = 0.0; r.ka = 0.0; r.b0 = 0.0; r.b1 = 0.0;
+  r.rd_us = 0; r.rd_acc = 0; r.wr_acc = 0; r.to_u = 0;
+  if (scheme == HD_SCHEME_RK4) {
+    switch (stage) {
+      case 0: r.kc = 0.5; r.b1 = 1.0; r.wr_acc = 1; break;                       // acc = k1
+      case 1: r.kc = 0.5; r.b0 = 1.0; r.b1 = 2.0; r.rd_acc = r.wr_acc = 1; break;  // acc += 2 k2
+      case 2: r.kc = 1.0; r.b0 = 1.0; r.b1 = 2.0; r.rd_acc = r.wr_acc = 1; break;  // acc += 2 k3
+      default: r.kc = r.ka = 1.0 / 6.0; r.rd_acc = 1; r.to_u = 1; break;          // u + dt/6 (acc + k4)
+    }
+  } else {
+    switch (stage) {
+      case 0: r.kc = 1.0; break;
+      case 1: r.a0 = 0.75; r.a1 = 0.25; r.kc = 0.25; r.rd_us = 1; break;
+      default: r.a0 = 1.0 / 3.0; r.a1 = 2.0 / 3.0; r.kc = 2.0 / 3.0; r.rd_us = 1; r.to_u = 1; break;
+    }
+  }
   return r;
 }
 

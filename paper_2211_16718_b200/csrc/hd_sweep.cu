@@ -17,7 +17,9 @@
 // inc read-modify-write is a fully coalesced 256-byte warp access.
 // x sweep: lanes are consecutive y rows; each lane walks its row sequentially
 // (sector reuse through L1).
-#include "hd_internal.cuh"
+#include <cstring>
+
+#include "hd_device.cuh"
 
 namespace hd {
 
@@ -67,15 +69,20 @@ __device__ __forceinline__ void recon_pair(double q0, double q1, double q2, doub
     left = recon5_exact(q0, q1, q2, q3, q4, eps, power);
     right = recon5_exact(q4, q3, q2, q1, q0, eps, power);
   } else {
-    const double t1 = (q0 - 2.0 * q1) + q2;
-    const double s1 = (q0 - 4.0 * q1) + 3.0 * q2;
-    const double t2 = (q1 - 2.0 * q2) + q3;
-    const double s2 = q1 - q3;
-    const double t3 = (q2 - 2.0 * q3) + q4;
-    const double s3 = (3.0 * q2 - 4.0 * q3) + q4;
-    const double d1 = fma(C13_12 * t1, t1, fma(0.25 * s1, s1, eps));
-    const double d2 = fma(C13_12 * t2, t2, fma(0.25 * s2, s2, eps));
-    const double d3 = fma(C13_12 * t3, t3, fma(0.25 * s3, s3, eps));
+    // Everything in first differences D_i = q_{i+1} - q_i of the window:
+    //   beta_k = 13/12 t_k^2 + 1/4 s_k^2 with t1 = D1-D0, s1 = 3D1-D0, t2 = D2-D1,
+    //   s2 = -(D1+D2), t3 = D3-D2, s3 = D3-3D2 (scaled by 12; the common factor
+    //   cancels in the normalised weights once eps is scaled too), and since the
+    //   weights sum to one each value is q2 + sum_k w_k (c_k - q2), with
+    //   6 (c_k - q2) = 5D1-2D0, D1+2D2, 4D2-D3 (left) and 2D3-5D2, -(D2+2D1),
+    //   D0-4D1 (right).
+    const double D0 = q1 - q0, D1 = q2 - q1, D2 = q3 - q2, D3 = q4 - q3;
+    const double t1 = D1 - D0, t2 = D2 - D1, t3 = D3 - D2;
+    const double s1 = fma(3.0, D1, -D0), s2 = D1 + D2, s3 = fma(-3.0, D2, D3);
+    const double eps12 = 12.0 * eps;
+    const double d1 = fma(13.0 * t1, t1, fma(3.0 * s1, s1, eps12));
+    const double d2 = fma(13.0 * t2, t2, fma(3.0 * s2, s2, eps12));
+    const double d3 = fma(13.0 * t3, t3, fma(3.0 * s3, s3, eps12));
     double e1 = d1, e2 = d2, e3 = d3;
     for (int q = 0; q < power - 1; ++q) {
       e1 *= d1;
@@ -86,16 +93,12 @@ __device__ __forceinline__ void recon_pair(double q0, double q1, double q2, doub
     const double mid = 6.0 * e13;  // 0.6/e2 weight, both sides (x10 scaling cancels)
     // left: (0.1/e1, 0.6/e2, 0.3/e3) ~ (e23, 6 e13, 3 e12)
     const double nl1 = e23, nl3 = 3.0 * e12;
-    const double cl1 = fma(C11_6, q2, fma(C1_3, q0, -C7_6 * q1));
-    const double cl2 = fma(C1_3, q3, fma(C5_6, q2, -C1_6 * q1));
-    const double cl3 = fma(C1_3, q2, fma(C5_6, q3, -C1_6 * q4));
-    left = fma(nl1, cl1, fma(mid, cl2, nl3 * cl3)) * frcp((nl1 + mid) + nl3);
+    const double al1 = fma(5.0, D1, -2.0 * D0), al2 = fma(2.0, D2, D1), al3 = fma(4.0, D2, -D3);
+    left = fma(fma(nl1, al1, fma(mid, al2, nl3 * al3)), frcp(6.0 * ((nl1 + mid) + nl3)), q2);
     // right (mirrored): (0.1/e3, 0.6/e2, 0.3/e1) ~ (e12, 6 e13, 3 e23)
     const double nr1 = e12, nr3 = 3.0 * e23;
-    const double cr1 = fma(C11_6, q2, fma(C1_3, q4, -C7_6 * q3));
-    const double cr2 = fma(C1_3, q1, fma(C5_6, q2, -C1_6 * q3));
-    const double cr3 = fma(C1_3, q2, fma(C5_6, q1, -C1_6 * q0));
-    right = fma(nr1, cr1, fma(mid, cr2, nr3 * cr3)) * frcp((nr1 + mid) + nr3);
+    const double ar1 = fma(-5.0, D2, 2.0 * D3), ar2 = fma(2.0, D1, D2), ar3 = fma(-4.0, D1, D0);
+    right = fma(fma(nr1, ar1, fma(-mid, ar2, nr3 * ar3)), frcp(6.0 * ((nr1 + mid) + nr3)), q2);
   }
 }
 
@@ -246,16 +249,16 @@ __device__ __forceinline__ void roe_flux(const double (&uL)[NV], const double (&
 // ---------------------------------------------------------------------------
 template <int DIM, bool EXACT>
 __device__ __forceinline__ void point_flux(const double (&u)[NV], double gm1, double (&f)[NV],
-                                           double& rho_out, double& p_out) {
-  double vx, vy, vz, p;
+                                           double& inv_out, double (&prim)[4]) {
+  double vx, vy, vz, p, inv;
   if constexpr (EXACT) {
-    const double inv = xd(1.0, u[0]);
+    inv = xd(1.0, u[0]);
     vx = xm(u[1], inv);
     vy = xm(u[2], inv);
     vz = xm(u[3], inv);
     p = xm(gm1, xs(u[4], xm(xm(0.5, u[0]), xa(xa(xm(vx, vx), xm(vy, vy)), xm(vz, vz)))));
   } else {
-    const double inv = frcp(u[0]);
+    inv = frcp(u[0]);
     vx = u[1] * inv;
     vy = u[2] * inv;
     vz = u[3] * inv;
@@ -276,8 +279,11 @@ __device__ __forceinline__ void point_flux(const double (&u)[NV], double gm1, do
     f[1 + DIM] += p;
     f[4] = (u[4] + p) * vd;
   }
-  rho_out = u[0];
-  p_out = p;
+  inv_out = inv;
+  prim[0] = vx;
+  prim[1] = vy;
+  prim[2] = vz;
+  prim[3] = p;
 }
 
 constexpr int SWEEP_THREADS = 64;
@@ -285,6 +291,16 @@ constexpr int SWEEP_THREADS = 64;
 #define HD_SWEEP_MIN_BLOCKS 4
 #endif
 constexpr int SWEEP_MIN_BLOCKS = HD_SWEEP_MIN_BLOCKS;  // blocks of 64 threads per SM (register cap)
+
+// What a sweep does besides -dF/dx (the fused stage pipeline, hd_api.cu):
+//   ROLE_PLAIN  inc (-)= dF/dx
+//   ROLE_PRIMS  y sweep: also stores the viscous primitives (u, v, w, T) of the
+//               points it owns (coalesced: lanes are consecutive x), plus their face
+//               images along locally periodic axes
+//   ROLE_UPDATE z sweep (fast mode, last kernel of a stage): the finished
+//               increment (viscous divergence already added) feeds the RK stage
+//               update (timeint.py:168-193) instead of being stored
+constexpr int ROLE_PLAIN = 0, ROLE_PRIMS = 1, ROLE_UPDATE = 2;
 
 struct SweepArgs {
   Geo geo;
@@ -297,40 +313,50 @@ struct SweepArgs {
   int check;        // latch positivity of interior points
   unsigned long long* err;
   int64_t tag;
+  // ROLE_PRIMS
+  double* prim;
+  // ROLE_UPDATE
+  RKArgs rk;
 };
 
-// Line geometry: thread -> (line origin pointer offset, stride, transverse ok)
+// Line geometry: thread -> interior coords of the line origin
 template <int DIM>
-__device__ __forceinline__ bool line_of(const SweepArgs& a, int64_t& base, int& seg_id) {
+__device__ __forceinline__ bool line_of(const SweepArgs& a, int& i, int& j, int& k) {
   const Geo& G = a.geo;
-  int i, j, k;
   if (DIM == 0) {
     j = blockIdx.x * blockDim.x + threadIdx.x;
     k = blockIdx.y * blockDim.y + threadIdx.y;
-    if (j >= G.n[1] || k >= G.n[2]) return false;
     i = 0;
+    return j < G.n[1] && k < G.n[2];
   } else if (DIM == 1) {
     i = blockIdx.x * blockDim.x + threadIdx.x;
     k = blockIdx.y * blockDim.y + threadIdx.y;
-    if (i >= G.n[0] || k >= G.n[2]) return false;
     j = 0;
+    return i < G.n[0] && k < G.n[2];
   } else {
     i = blockIdx.x * blockDim.x + threadIdx.x;
     j = blockIdx.y * blockDim.y + threadIdx.y;
-    if (i >= G.n[0] || j >= G.n[1]) return false;
     k = 0;
+    return i < G.n[0] && j < G.n[1];
   }
-  base = G.idx(i, j, k);
-  seg_id = blockIdx.z;
-  return true;
 }
 
-template <int DIM, bool EXACT>
+// The viscous primitives (u, v, w, T) of point (i, j, k) and their face images
+// along the locally periodic axes (the gradient stencils are axis-aligned).
+__device__ __forceinline__ void store_prim(double* prim, const Geo& G, int i, int j, int k,
+                                           const double (&pv)[4]) {
+  const int mask = (G.periodic[0] ? 1 : 0) | (G.periodic[1] ? 2 : 0) | (G.periodic[2] ? 4 : 0);
+#pragma unroll
+  for (int f = 0; f < 4; ++f) store_face_images(prim + f * G.npts, G, i, j, k, mask, pv[f]);
+}
+
+template <int DIM, bool EXACT, int ROLE>
 __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(const SweepArgs a) {
-  int64_t base;
-  int seg_id;
-  if (!line_of<DIM>(a, base, seg_id)) return;
+  int li, lj, lk;
+  if (!line_of<DIM>(a, li, lj, lk)) return;
   const Geo& G = a.geo;
+  const int64_t base = G.idx(li, lj, lk);
+  const int seg_id = blockIdx.z;
   const int nd = G.n[DIM];
   const int c0 = seg_id * a.seg;
   if (c0 >= nd) return;
@@ -356,11 +382,19 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(
   auto ingest = [&](int m, const double (&src)[NV], double (&uu)[NV], double (&ff)[NV]) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) uu[v] = src[v];
-    double rho, p;
-    point_flux<DIM, EXACT>(uu, gm1, ff, rho, p);
+    double inv, pv[4];
+    point_flux<DIM, EXACT>(uu, gm1, ff, inv, pv);
     if (a.check && m >= 0 && m < nd) {
-      if (!(rho > 0.0)) latch_error(a.err, a.tag, 1, base + (int64_t)m * sd);
-      else if (!(p > 0.0)) latch_error(a.err, a.tag, 2, base + (int64_t)m * sd);
+      if (!(uu[0] > 0.0)) latch_error(a.err, a.tag, 1, base + (int64_t)m * sd);
+      else if (!(pv[3] > 0.0)) latch_error(a.err, a.tag, 2, base + (int64_t)m * sd);
+    }
+    if constexpr (ROLE == ROLE_PRIMS) {
+      if (a.prim && m >= c0 && m < c1) {
+        // viscous.py:80-81: T = gamma p / rho
+        if constexpr (EXACT) pv[3] = xd(xm(a.ph.gamma, pv[3]), uu[0]);
+        else pv[3] = a.ph.gamma * pv[3] * inv;
+        store_prim(a.prim, G, DIM == 0 ? m : li, DIM == 1 ? m : lj, DIM == 2 ? m : lk, pv);
+      }
     }
   };
 
@@ -388,6 +422,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(
     if (c < c1) fetch(c + 3, pre);
     const bool wr = c > c0;
     double* q = inc + (int64_t)(c - 1) * sd;
+    // ROLE_UPDATE: the RK inputs of cell c-1 (base state, accumulator) are
+    // loaded here, a full window of FP64 work before the update consumes them
+    double ru0[NV], racc[NV];
+    if constexpr (ROLE == ROLE_UPDATE) {
+      const int64_t qo = base + (int64_t)(c - 1) * sd;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        ru0[v] = wr ? a.rk.u[qo + v * np] : 0.0;
+        racc[v] = (wr && a.rk.rd_acc) ? a.rk.acc[qo + v * np] : 0.0;
+      }
+    }
     double old[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) old[v] = (wr && a.accumulate) ? q[v * np] : 0.0;
@@ -405,14 +450,22 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(
       double flux[NV];
       roe_flux<DIM, EXACT>(lu, ru, lf, rf, a.ph, flux);
       if (wr) {
+        double val[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           // accumulate: inc -= d ; first sweep of an RHS: inc = 0 - d (upwind.py:181-182)
-          if constexpr (EXACT) {
-            q[v * np] = xs(old[v], xm(xs(flux[v], fprev[v]), a.inv_dx));
-          } else {
-            q[v * np] = old[v] - (flux[v] - fprev[v]) * a.inv_dx;
-          }
+          if constexpr (EXACT) val[v] = xs(old[v], xm(xs(flux[v], fprev[v]), a.inv_dx));
+          else val[v] = old[v] - (flux[v] - fprev[v]) * a.inv_dx;
+        }
+        if constexpr (ROLE == ROLE_UPDATE) {
+          int ci = li, cj = lj, ck = lk;
+          if (DIM == 0) ci = c - 1;
+          else if (DIM == 1) cj = c - 1;
+          else ck = c - 1;
+          rk_store_pre(a.rk, G, ci, cj, ck, val, ru0, racc);
+        } else {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) q[v * np] = val[v];
         }
       }
 #pragma unroll
@@ -426,29 +479,29 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(
   }
 }
 
-template <int DIM, bool EXACT>
+template <int DIM, bool EXACT, int ROLE>
 static int launch_dim(const hd_plan* p, const SweepArgs& a, int nseg, cudaStream_t s) {
   const Geo& G = p->geo;
-  dim3 block, grid;
   constexpr int BY = SWEEP_THREADS / 32;
-  block = dim3(32, BY, 1);
+  dim3 block(32, BY, 1), grid;
   if (DIM == 0) grid = dim3((G.n[1] + 31) / 32, (G.n[2] + BY - 1) / BY, nseg);
   else if (DIM == 1) grid = dim3((G.n[0] + 31) / 32, (G.n[2] + BY - 1) / BY, nseg);
   else grid = dim3((G.n[0] + 31) / 32, (G.n[1] + BY - 1) / BY, nseg);
-  sweep_kernel<DIM, EXACT><<<grid, block, 0, s>>>(a); hd::count_launches(1);
+  sweep_kernel<DIM, EXACT, ROLE><<<grid, block, 0, s>>>(a);
+  hd::count_launches(1);
   return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
 }
 
-int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int accumulate, int check,
-                 int64_t tag, cudaStream_t s) {
-  if (dim < 0 || dim > 2) return HD_E_ARG;
+static SweepArgs make_args(const hd_plan* p, int dim, const double* u, double* inc, int accumulate,
+                           int check, int64_t tag, int& nseg) {
   const Geo& G = p->geo;
   SweepArgs a;
+  memset(&a, 0, sizeof(a));
   a.geo = G;
   a.ph = p->phys;
   a.u = u;
   a.inc = inc;
-  a.inv_dx = 1.0 / G.h[dim];
+  a.inv_dx = 1.0 / G.h[dim];  // upwind.py:204
   a.accumulate = accumulate;
   a.check = check;
   a.err = (unsigned long long*)(p->ws + p->off[HD_BUF_ERR]);
@@ -456,20 +509,46 @@ int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int ac
   // segment length: enough independent lines to fill ~6 waves of 148 SMs x 256 threads
   const int64_t lines = (int64_t)G.n[0] * G.n[1] * G.n[2] / G.n[dim];
   const int64_t target = (int64_t)p->sm_count * 256 * 6;
-  int nseg = (int)((target + lines - 1) / lines);
+  nseg = (int)((target + lines - 1) / lines);
   if (nseg < 1) nseg = 1;
   if (nseg > G.n[dim] / 8) nseg = G.n[dim] / 8 > 0 ? G.n[dim] / 8 : 1;
   a.seg = (G.n[dim] + nseg - 1) / nseg;
   nseg = (G.n[dim] + a.seg - 1) / a.seg;
+  return a;
+}
+
+int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int accumulate, int check,
+                 int64_t tag, cudaStream_t s) {
+  if (dim < 0 || dim > 2) return HD_E_ARG;
+  int nseg;
+  SweepArgs a = make_args(p, dim, u, inc, accumulate, check, tag, nseg);
   const bool exact = p->mode == HD_MODE_EXACT;
   switch (dim * 2 + (exact ? 1 : 0)) {
-    case 0: return launch_dim<0, false>(p, a, nseg, s);
-    case 1: return launch_dim<0, true>(p, a, nseg, s);
-    case 2: return launch_dim<1, false>(p, a, nseg, s);
-    case 3: return launch_dim<1, true>(p, a, nseg, s);
-    case 4: return launch_dim<2, false>(p, a, nseg, s);
-    default: return launch_dim<2, true>(p, a, nseg, s);
+    case 0: return launch_dim<0, false, ROLE_PLAIN>(p, a, nseg, s);
+    case 1: return launch_dim<0, true, ROLE_PLAIN>(p, a, nseg, s);
+    case 2: return launch_dim<1, false, ROLE_PLAIN>(p, a, nseg, s);
+    case 3: return launch_dim<1, true, ROLE_PLAIN>(p, a, nseg, s);
+    case 4: return launch_dim<2, false, ROLE_PLAIN>(p, a, nseg, s);
+    default: return launch_dim<2, true, ROLE_PLAIN>(p, a, nseg, s);
   }
+}
+
+int launch_sweep_prims(const hd_plan* p, const double* u, double* inc, double* prim, int64_t tag,
+                       cudaStream_t s) {
+  int nseg;
+  SweepArgs a = make_args(p, 1, u, inc, 1, 0, tag, nseg);
+  a.prim = prim;
+  if (p->mode == HD_MODE_EXACT) return HD_E_UNSUPPORTED;  // exact mode runs the unfused stage
+  return launch_dim<1, false, ROLE_PRIMS>(p, a, nseg, s);
+}
+
+int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, int scheme, int stage,
+                        double* u, const double* dt_dev, int64_t tag, cudaStream_t s) {
+  int nseg;
+  SweepArgs a = make_args(p, 2, u_stage, inc, 1, 0, tag, nseg);
+  a.rk = make_rk(p, scheme, stage, u, dt_dev);
+  if (p->mode == HD_MODE_EXACT) return HD_E_UNSUPPORTED;  // exact mode runs the unfused stage
+  return launch_dim<2, false, ROLE_UPDATE>(p, a, nseg, s);
 }
 
 }  // namespace hd

@@ -12,8 +12,8 @@ replaced by torch.distributed over NCCL/NVLink:
   (``batch_isend_irecv``) right after the previous stage's update kernel and
   overlaps the x and y sweeps, which never read z ghosts; the z sweep waits
   on it (``hd_stage_part`` HD_PART_LOCAL / HD_PART_HALO);
-* the viscous flux faces of the z-direction flux group are exchanged while
-  the x/y flux divergence runs (HD_PART_DIVLOC / HD_PART_UPDATE);
+* the viscous flux faces of the z-differentiated flux group (4 of the 9
+  symmetric flux fields, g planes) are exchanged before the divergence;
 * the CFL signal and diagnostics are combined with ``all_reduce`` (MAX for
   signals, SUM for totals) on device tensors -- dt never leaves HBM.
 
@@ -258,23 +258,23 @@ class DistHalo:
         plan = get_plan(spec, gas, weno_params, delta, mode, periodic=self.periodic)
         scheme = _SCHEME_CODE[tparams.scheme]
         nst = 3 if scheme == _lib.HD_SCHEME_RK3 else 4
-        stage_buf = plan.fields(_lib.HD_BUF_STAGE, NVARS)
-        vflux_z = plan.fields(_lib.HD_BUF_VFLUX, 12)[8 * spec.total_points:]
+        stage_buf = plan.fields(_lib.HD_BUF_STAGE, 2 * NVARS)  # ping-pong halves
+        half = NVARS * spec.total_points
+        vflux_z = plan.fields(_lib.HD_BUF_VFLUX, 9)[5 * spec.total_points:]  # the z group
         visc = gas.effective_mu != 0.0
         halo = self
 
         def stepper(u, dt_dev, tag):
             plan.fill_ghosts(u, NVARS)  # x/y wrap of the step input (z: exchanged below)
             for s in range(nst):
-                us = u if s == 0 else stage_buf
-                works = halo.exchange_z_async(us, NVARS, spec)
+                us = u if s == 0 else stage_buf[((s - 1) % 2) * half: ((s - 1) % 2 + 1) * half]
+                works = halo.exchange_z_async(us, NVARS, spec)   # overlaps the x/y sweeps
                 plan.stage_part(scheme, s, _lib.HD_PART_LOCAL, u, dt_dev, tag)
                 halo.wait(works)
                 plan.stage_part(scheme, s, _lib.HD_PART_HALO, u, dt_dev, tag)
-                works = halo.exchange_z_async(vflux_z, 4, spec) if visc else []
-                plan.stage_part(scheme, s, _lib.HD_PART_DIVLOC, u, dt_dev, tag)
-                halo.wait(works)
-                plan.stage_part(scheme, s, _lib.HD_PART_UPDATE, u, dt_dev, tag)
+                if visc:
+                    halo.wait(halo.exchange_z_async(vflux_z, 4, spec))
+                plan.stage_part(scheme, s, _lib.HD_PART_DIV | _lib.HD_PART_UPDATE, u, dt_dev, tag)
 
         def reducer(red):
             if halo.layout.dims[2] > 1:

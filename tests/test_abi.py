@@ -47,7 +47,7 @@ def test_workspace_size_is_host_only():
         g.periodic[d] = 1
     g.ghost = 3
     nbytes = lib.hd_workspace_bytes(ctypes.byref(g))
-    assert nbytes >= 31 * 22 ** 3 * 8
+    assert nbytes >= 33 * 22 ** 3 * 8
     g.ghost = 2
     assert lib.hd_workspace_bytes(ctypes.byref(g)) == -1
 
