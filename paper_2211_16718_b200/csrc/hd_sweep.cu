@@ -287,10 +287,25 @@ __device__ __forceinline__ void point_flux(const double (&u)[NV], double gm1, do
 }
 
 constexpr int SWEEP_THREADS = 64;
-#ifndef HD_SWEEP_MIN_BLOCKS
-#define HD_SWEEP_MIN_BLOCKS 4
+// Window placement and register cap per sweep direction (measured on B200 at
+// 512^3, tools/sweep_bench.py):
+//   y, z: window in shared memory, 6 blocks of 64 threads per SM (12 warps,
+//         <= 168 registers, no spills) -- 7.3 ms vs 8.3 ms with a register window
+//   x:    register window, 4 blocks per SM -- its lanes walk different rows, and
+//         more resident warps thrash L1 (15.5 ms at 6 blocks vs 9.9 ms)
+#ifndef HD_SWEEP_SMEM_WINDOW_YZ
+#define HD_SWEEP_SMEM_WINDOW_YZ 1
 #endif
-constexpr int SWEEP_MIN_BLOCKS = HD_SWEEP_MIN_BLOCKS;  // blocks of 64 threads per SM (register cap)
+#ifndef HD_SWEEP_MIN_BLOCKS_YZ
+#define HD_SWEEP_MIN_BLOCKS_YZ 6
+#endif
+#ifndef HD_SWEEP_MIN_BLOCKS_X
+#define HD_SWEEP_MIN_BLOCKS_X 4
+#endif
+template <int DIM> struct SweepCfg {
+  static constexpr bool smem_window = DIM != 0 && HD_SWEEP_SMEM_WINDOW_YZ;
+  static constexpr int min_blocks = DIM == 0 ? HD_SWEEP_MIN_BLOCKS_X : HD_SWEEP_MIN_BLOCKS_YZ;
+};
 
 // What a sweep does besides -dF/dx (the fused stage pipeline, hd_api.cu):
 //   ROLE_PLAIN  inc (-)= dF/dx
@@ -351,7 +366,8 @@ __device__ __forceinline__ void store_prim(double* prim, const Geo& G, int i, in
 }
 
 template <int DIM, bool EXACT, int ROLE>
-__global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) sweep_kernel(const SweepArgs a) {
+  constexpr bool SMEM_WINDOW = SweepCfg<DIM>::smem_window;
   int li, lj, lk;
   if (!line_of<DIM>(a, li, lj, lk)) return;
   const Geo& G = a.geo;
@@ -368,7 +384,14 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(
   const double gm1 = a.ph.gm1, eps = a.ph.eps;
   const int power = a.ph.power;
 
-  // window: point w holds line position c - 2 + w (w = 0..4)
+  // Window in shared memory (SMEM_WINDOW): a 5-slot ring per thread, slot =
+  // position mod 5, 9 values per point (u0..u4, f1..f4; f0 == u_{1+dim});
+  // consecutive threads hold consecutive doubles, so every access is bank-
+  // conflict free, and the 45-double window stays out of the register file.
+  // Otherwise a register window: point w holds line position c - 2 + w.
+  __shared__ double ring[SMEM_WINDOW ? 5 * 9 * SWEEP_THREADS : 1];
+  double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
+  auto slot = [&](int m) -> double* { return mine + ((m + 5) % 5) * (9 * SWEEP_THREADS); };
   double wu[5][NV], wf[5][NV];
 
   // raw loads are issued one iteration before the point enters the window
@@ -384,6 +407,13 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(
     for (int v = 0; v < NV; ++v) uu[v] = src[v];
     double inv, pv[4];
     point_flux<DIM, EXACT>(uu, gm1, ff, inv, pv);
+    if constexpr (SMEM_WINDOW) {
+      double* sp = slot(m);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sp[v * SWEEP_THREADS] = uu[v];
+#pragma unroll
+      for (int v = 1; v < NV; ++v) sp[(NV - 1 + v) * SWEEP_THREADS] = ff[v];
+    }
     if (a.check && m >= 0 && m < nd) {
       if (!(uu[0] > 0.0)) latch_error(a.err, a.tag, 1, base + (int64_t)m * sd);
       else if (!(pv[3] > 0.0)) latch_error(a.err, a.tag, 2, base + (int64_t)m * sd);
@@ -410,12 +440,14 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(
   double fprev[NV];
   for (int c = c0 - 1; c <= c1; ++c) {
     // shift; position c+2 enters from the prefetch buffer
+    if constexpr (!SMEM_WINDOW) {
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
+      for (int w = 0; w < 4; ++w) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        wu[w][v] = wu[w + 1][v];
-        wf[w][v] = wf[w + 1][v];
+        for (int v = 0; v < NV; ++v) {
+          wu[w][v] = wu[w + 1][v];
+          wf[w][v] = wf[w + 1][v];
+        }
       }
     }
     ingest(c + 2, pre, wu[4], wf[4]);
@@ -438,14 +470,30 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS) sweep_kernel(
     for (int v = 0; v < NV; ++v) old[v] = (wr && a.accumulate) ? q[v * np] : 0.0;
     // reconstructions of window c: ru/rf at c-1/2, nu/nf at c+1/2
     double ru[NV], rf[NV], nu[NV], nf[NV];
+    if constexpr (SMEM_WINDOW) {
+      const double* w0 = slot(c - 2);
+      const double* w1 = slot(c - 1);
+      const double* w2 = slot(c);
+      const double* w3 = slot(c + 1);
+      const double* w4 = slot(c + 2);
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
-      recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
+      for (int v = 0; v < 2 * NV - 1; ++v) {
+        double l, r;
+        recon_pair<EXACT>(w0[v * SWEEP_THREADS], w1[v * SWEEP_THREADS], w2[v * SWEEP_THREADS],
+                          w3[v * SWEEP_THREADS], w4[v * SWEEP_THREADS], eps, power, l, r);
+        if (v < NV) { nu[v] = l; ru[v] = r; }
+        else { nf[v - NV + 1] = l; rf[v - NV + 1] = r; }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
+#pragma unroll
+      for (int v = 1; v < NV; ++v)
+        recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
+    }
     nf[0] = nu[1 + DIM];
     rf[0] = ru[1 + DIM];
-#pragma unroll
-    for (int v = 1; v < NV; ++v)
-      recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
     if (c >= c0) {
       double flux[NV];
       roe_flux<DIM, EXACT>(lu, ru, lf, rf, a.ph, flux);

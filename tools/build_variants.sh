@@ -1,14 +1,19 @@
 #!/bin/bash
-# Build libhd.so variants with different sweep register caps into build/variants/
+# Build libhd.so variants into build/variants/<name>/ ; each arg is name:DEFINES (comma-separated)
+#   tools/build_variants.sh reg4:HD_SWEEP_MIN_BLOCKS=4 smem5:HD_SWEEP_SMEM_WINDOW=1,HD_SWEEP_MIN_BLOCKS=5
 set -e
 cd "$(dirname "$0")/../paper_2211_16718_b200/csrc"
-mkdir -p ../../build/variants
-for mb in "$@"; do
-  out=../../build/variants/mb$mb
+for spec in "$@"; do
+  name=${spec%%:*}
+  defs=""
+  IFS=',' read -ra kv <<< "${spec#*:}"
+  for d in "${kv[@]}"; do defs="$defs -D$d"; done
+  out=../../build/variants/$name
   mkdir -p $out
   for f in hd_sweep hd_field hd_api; do
-    /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -DHD_SWEEP_MIN_BLOCKS=$mb -c $f.cu -o $out/$f.o &
+    /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $defs -Xptxas -v -c $f.cu -o $out/$f.o 2> $out/$f.ptxas.log &
   done
   wait
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libhd.so $out/*.o -lcudart
+  echo "$name: $(grep -c spill $out/hd_sweep.ptxas.log) kernels, spills: $(grep 'spill' $out/hd_sweep.ptxas.log | grep -v ' 0 bytes spill stores' | wc -l)"
 done

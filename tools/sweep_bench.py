@@ -44,3 +44,14 @@ e1.record()
 torch.cuda.synchronize()
 out["viscous_ms"] = e0.elapsed_time(e1) / a.reps
 print(json.dumps(out))
+tp = hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=1)
+res = hd.advance(ic, gas, tp)
+torch.cuda.synchronize()
+tp = hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=3)
+e0.record()
+res = hd.advance(res.fields, gas, tp)
+e1.record()
+torch.cuda.synchronize()
+out["step_ms"] = e0.elapsed_time(e1) / 3
+out["pt_step_per_s"] = a.n ** 3 / (out["step_ms"] / 1e3)
+print(json.dumps(out))
