@@ -174,11 +174,12 @@ def time_kernels(hd, torch, plan, u, reps=3):
     res = {}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for dim, name in enumerate(("sweep_x", "sweep_y", "sweep_z")):
-        plan.hyper_sweep(dim, u, inc, True)
+        acc = dim != 0  # as in the stage pipeline: the x sweep overwrites inc, y/z accumulate
+        plan.hyper_sweep(dim, u, inc, acc)
         torch.cuda.synchronize()
         e0.record()
         for _ in range(reps):
-            plan.hyper_sweep(dim, u, inc, True)
+            plan.hyper_sweep(dim, u, inc, acc)
         e1.record()
         torch.cuda.synchronize()
         res[name] = e0.elapsed_time(e1) / reps
@@ -273,7 +274,8 @@ def main():
     hbm_peak = float(peaks["hbm_gbs"])
     top = max(("sweep_x", "sweep_y", "sweep_z"), key=lambda k: kern[k])
     lpts = lspec.interior_points
-    sweep_bytes = lpts * 120.0  # read u (40 B) + inc read-modify-write (80 B) per point
+    # read u (40 B) + inc write (x: 40 B) or read-modify-write (y, z: 80 B) per point
+    sweep_bytes = lpts * (80.0 if top == "sweep_x" else 120.0)
     sweep_flops = lpts * SWEEP_FLOPS_PER_PT
     achieved_gbs = sweep_bytes / (kern[top] / 1e3) / 1e9
     traffic = None

@@ -90,19 +90,17 @@ def decompose(spec: GridSpec, dims) -> list:
 
 
 def default_dims(nranks: int, n, ghost_width: int = 3):
-    """GPU choice: split z first, then y (contiguous faces, no packing).
+    """GPU choice: split z only -> (1, 1, nranks).
 
-    The reference prefers x splits to minimise face area on CPUs
-    (decomp.py:106-140); results are decomposition-invariant, so this is a
-    pure performance choice."""
-    for dy in range(1, nranks + 1):
-        if nranks % dy:
-            continue
-        dz = nranks // dy
-        dims = (1, dy, dz)
-        if all(n[d] % dims[d] == 0 and n[d] // dims[d] >= ghost_width for d in range(3)):
-            return dims
-    raise ConfigError(f"no legal z/y decomposition of {n} into {nranks} ranks")
+    z faces are contiguous per variable (no pack kernels) and the x/y sweeps
+    overlap the exchange.  The reference prefers x splits to minimise face
+    area on CPUs (decomp.py:106-140); results are decomposition-invariant, so
+    this is a pure performance choice."""
+    dims = (1, 1, int(nranks))
+    if n[2] % nranks == 0 and n[2] // nranks >= ghost_width:
+        return dims
+    raise ConfigError(f"no legal z decomposition of {tuple(n)} into {nranks} ranks "
+                      f"(need n_z % ranks == 0 and n_z / ranks >= {ghost_width})")
 
 
 def comm_fraction(comm_seconds: float, busy_seconds: float) -> float:
