@@ -17,6 +17,7 @@
 // inc read-modify-write is a fully coalesced 256-byte warp access.
 // x sweep: lanes are consecutive y rows; each lane walks its row sequentially
 // (sector reuse through L1).
+#include <cstdlib>
 #include <cstring>
 
 #include "hd_device.cuh"
@@ -527,6 +528,163 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   }
 }
 
+// ---------------------------------------------------------------------------
+// x sweep with shared-memory staging.  A warp owns 32 consecutive y rows of one
+// z plane and marches them along x together; x is the contiguous axis, so the
+// plain kernel's per-lane loads and stores touch 32 different rows (one sector
+// per lane: partial-sector writes, L1 thrash).  Here the warp moves 4-point
+// chunks of all 32 rows with cp.async (lane l copies row 8i + l/4, position
+// l%4: four full 32-byte sectors per instruction), double-buffered one chunk
+// ahead, and its increments go out the same way through a staging tile.
+// ---------------------------------------------------------------------------
+static bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] && v[0] != '0';
+}
+
+constexpr int XS_PAD = 5;  // row pitch of a staging tile (doubles): 40 B, conflict-free 64-bit reads
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <bool EXACT>
+__global__ void __launch_bounds__(SWEEP_THREADS, HD_SWEEP_MIN_BLOCKS_X) sweep_x_staged_kernel(
+    const SweepArgs a) {
+  constexpr int WARPS = SWEEP_THREADS / 32;
+  __shared__ double xin[WARPS][2][NV][32 * XS_PAD];
+  __shared__ double xout[WARPS][NV][32 * XS_PAD];
+  const Geo& G = a.geo;
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const int j0 = blockIdx.x * 32;  // launch guarantees n_y % 32 == 0
+  const int k = blockIdx.y * WARPS + w;
+  if (k >= G.n[2]) return;  // warp-uniform
+  const int nd = G.n[0];
+  const int c0 = blockIdx.z * a.seg;
+  if (c0 >= nd) return;
+  const int c1 = min(c0 + a.seg, nd);
+  const int64_t np = G.npts;
+  const int64_t row0 = G.idx(0, j0, k);  // cell x = 0 of row j0
+  const int64_t sy = G.sy;
+  const int64_t base = row0 + (int64_t)lane * sy;  // this lane's row
+  const double gm1 = a.ph.gm1, eps = a.ph.eps;
+  const int power = a.ph.power;
+  const int p0 = c0 - 3;  // first position entering the window
+
+  // chunk t holds positions p0 + 4t .. p0 + 4t + 3 of all 32 rows
+  auto issue = [&](int t) {
+    const int buf = t & 1;
+    const int xo = lane & 3;
+    const int p = p0 + 4 * t + xo;
+    if (p <= c1 + 2) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 8 * i + (lane >> 2);
+        const double* src = a.u + row0 + (int64_t)r * sy + p;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) cp_async8(&xin[w][buf][v][r * XS_PAD + xo], src + v * np);
+      }
+    }
+    cp_async_commit();
+  };
+  auto take = [&](int p, double (&uu)[NV], double (&ff)[NV]) {
+    const int q = p - p0;
+    const double* s = &xin[w][(q >> 2) & 1][0][lane * XS_PAD + (q & 3)];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) uu[v] = s[v * 32 * XS_PAD];
+    double inv, pv[4];
+    point_flux<0, EXACT>(uu, gm1, ff, inv, pv);
+    if (a.check && p >= 0 && p < nd) {
+      if (!(uu[0] > 0.0)) latch_error(a.err, a.tag, 1, base + p);
+      else if (!(pv[3] > 0.0)) latch_error(a.err, a.tag, 2, base + p);
+    }
+  };
+  // out chunk: cells c0 + 4 t .. +3; d[v] staged, flushed coalesced as inc = old - d
+  auto flush = [&](int t) {
+    __syncwarp();
+    const int xo = lane & 3;
+    const int m = c0 + 4 * t + xo;
+    if (m < c1) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 8 * i + (lane >> 2);
+        double* dst = a.inc + row0 + (int64_t)r * sy + m;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double d = xout[w][v][r * XS_PAD + xo];
+          const double old = a.accumulate ? dst[v * np] : 0.0;
+          if constexpr (EXACT) dst[v * np] = xs(old, d);
+          else dst[v * np] = old - d;
+        }
+      }
+    }
+    __syncwarp();
+  };
+
+  double wu[5][NV], wf[5][NV];
+  issue(0);
+  issue(1);
+  cp_async_wait<1>();
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) take(p0 + q, wu[q + 1], wf[q + 1]);
+
+  double lu[NV], lf[NV], fprev[NV];
+  for (int c = c0 - 1; c <= c1; ++c) {
+    const int p = c + 2;
+    if (((p - p0) & 3) == 0) {  // entering chunk t: it has landed; start t+1
+      cp_async_wait<0>();
+      __syncwarp();
+      issue(((p - p0) >> 2) + 1);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        wu[q][v] = wu[q + 1][v];
+        wf[q][v] = wf[q + 1][v];
+      }
+    take(p, wu[4], wf[4]);
+    double ru[NV], rf[NV], nu[NV], nf[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+      recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
+#pragma unroll
+    for (int v = 1; v < NV; ++v)
+      recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
+    nf[0] = nu[1];
+    rf[0] = ru[1];
+    if (c >= c0) {
+      double flux[NV];
+      roe_flux<0, EXACT>(lu, ru, lf, rf, a.ph, flux);
+      if (c > c0) {
+        const int m = c - 1;
+        const int oo = (m - c0) & 3;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double d;
+          if constexpr (EXACT) d = xm(xs(flux[v], fprev[v]), a.inv_dx);
+          else d = (flux[v] - fprev[v]) * a.inv_dx;
+          xout[w][v][lane * XS_PAD + oo] = d;
+        }
+        if (oo == 3 || m == c1 - 1) flush((m - c0) >> 2);
+      }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) fprev[v] = flux[v];
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      lu[v] = nu[v];
+      lf[v] = nf[v];
+    }
+  }
+  cp_async_wait<0>();
+}
+
 template <int DIM, bool EXACT, int ROLE>
 static int launch_dim(const hd_plan* p, const SweepArgs& a, int nseg, cudaStream_t s) {
   const Geo& G = p->geo;
@@ -571,6 +729,15 @@ int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int ac
   int nseg;
   SweepArgs a = make_args(p, dim, u, inc, accumulate, check, tag, nseg);
   const bool exact = p->mode == HD_MODE_EXACT;
+  if (dim == 0 && p->geo.n[1] % 32 == 0 && !getenv_flag("HD_NO_XSTAGE")) {
+    constexpr int BY = SWEEP_THREADS / 32;
+    const Geo& G = p->geo;
+    dim3 block(32, BY, 1), grid(G.n[1] / 32, (G.n[2] + BY - 1) / BY, nseg);
+    if (exact) sweep_x_staged_kernel<true><<<grid, block, 0, s>>>(a);
+    else sweep_x_staged_kernel<false><<<grid, block, 0, s>>>(a);
+    hd::count_launches(1);
+    return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+  }
   switch (dim * 2 + (exact ? 1 : 0)) {
     case 0: return launch_dim<0, false, ROLE_PLAIN>(p, a, nseg, s);
     case 1: return launch_dim<0, true, ROLE_PLAIN>(p, a, nseg, s);

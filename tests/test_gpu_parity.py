@@ -243,3 +243,50 @@ def test_inviscid_conservation(hd):
     assert abs(m1 - m0) / abs(m0) < 1e-11
     assert abs(e1 - e0) / abs(e0) < 1e-11
     assert max(abs(a - b) for a, b in zip(mom0, mom1)) < 1e-11
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_x_sweep_staged_matches_unstaged(hd, oracle, monkeypatch, mode):
+    """The shared-memory staged x sweep (n_y % 32 == 0) is bitwise the plain x sweep,
+    and in exact mode bitwise the oracle (kernels.py:68-204 on x lines)."""
+    rng = np.random.default_rng(11)
+    P = oracle.Problem(n=(24, 64, 6), length=(1.0, 2.0, 0.5))
+    body = np.empty((5,) + (6, 64, 24))
+    rho = 0.6 + 0.8 * rng.random(body.shape[1:])
+    vel = 0.5 * rng.standard_normal((3,) + body.shape[1:])
+    p = 0.7 + 0.6 * rng.random(body.shape[1:])
+    body[0] = rho
+    body[1:4] = rho * vel
+    body[4] = p / 0.4 + 0.5 * rho * (vel ** 2).sum(0)
+    u = oracle.from_interior(body, P)
+    fs = _fs(hd, P, u)
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("HD_NO_XSTAGE", flag)
+        inc = fs.like()
+        inc.data.fill_(0.25)
+        hd.hyper_sweep(fs, 0, inc, mode=mode)
+        outs.append(inc.numpy())
+    assert np.array_equal(outs[0], outs[1])
+    if mode == "exact":
+        gz, gy, gx = P.shape
+        g = 3
+        flux = np.empty_like(u)
+        prim = u.reshape(5, -1)
+        inv = 1.0 / prim[0]
+        vx = prim[1] * inv
+        pp = (1.4 - 1.0) * (prim[4] - 0.5 * prim[0] * ((vx * vx + (prim[2] * inv) ** 2) + (prim[3] * inv) ** 2))
+        f = flux.reshape(5, -1)
+        f[0] = prim[1]
+        f[1] = prim[1] * vx + pp
+        f[2] = prim[2] * vx
+        f[3] = prim[3] * vx
+        f[4] = (prim[4] + pp) * vx
+        want = np.full_like(u, 0.25)
+        want.reshape(5, *P.shape)[:, :g] = 0.25
+        ref = np.zeros_like(u)
+        ref[:] = 0.25
+        oracle.hyper_sweep(u, flux, ref, P.npts, g * gx * gy + g * gx + g, 1, gx * gy, gx, 24, 64,
+                           0, 6, 0, 1.0 / (1.0 / 24), 1.4, 1e-6, 2, 0.0)
+        inner = oracle.interior
+        assert np.array_equal(inner(outs[0], P), inner(ref, P))
