@@ -283,7 +283,7 @@ def main():
     if os.path.exists(tfile):
         with open(tfile) as fh:
             tr = json.load(fh)
-        if tr.get("n") == n and tr.get("kernel") == top:
+        if tr.get("n") == n and world == 1 and tr.get("kernel") == top:
             traffic = tr.get("bytes_per_launch")
     roofline = {
         "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",

@@ -45,6 +45,19 @@ __device__ __forceinline__ double frcp(double x) {
   return fma(r, e, r);
 }
 
+// Reciprocal for the WENO weight normalisation: one Newton step.  It only
+// scales the correction term sum_k w_k (c_k - q2) (recon_pair), so its relative
+// error (~1e-14) enters the reconstructed value scaled by |c_k - q2| / |q2|.
+__device__ __forceinline__ double frcp_weights(double x) {
+#ifdef HD_WEIGHT_RCP_NEWTON2
+  return frcp(x);
+#else
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
+#endif
+}
+
 // Geometry of one plan, passed by value to every kernel.
 struct Geo {
   int n[3];     // interior extents (x, y, z)

@@ -95,11 +95,11 @@ __device__ __forceinline__ void recon_pair(double q0, double q1, double q2, doub
     // left: (0.1/e1, 0.6/e2, 0.3/e3) ~ (e23, 6 e13, 3 e12)
     const double nl1 = e23, nl3 = 3.0 * e12;
     const double al1 = fma(5.0, D1, -2.0 * D0), al2 = fma(2.0, D2, D1), al3 = fma(4.0, D2, -D3);
-    left = fma(fma(nl1, al1, fma(mid, al2, nl3 * al3)), frcp(6.0 * ((nl1 + mid) + nl3)), q2);
+    left = fma(fma(nl1, al1, fma(mid, al2, nl3 * al3)), frcp_weights(6.0 * ((nl1 + mid) + nl3)), q2);
     // right (mirrored): (0.1/e3, 0.6/e2, 0.3/e1) ~ (e12, 6 e13, 3 e23)
     const double nr1 = e12, nr3 = 3.0 * e23;
     const double ar1 = fma(-5.0, D2, 2.0 * D3), ar2 = fma(2.0, D1, D2), ar3 = fma(-4.0, D1, D0);
-    right = fma(fma(nr1, ar1, fma(-mid, ar2, nr3 * ar3)), frcp(6.0 * ((nr1 + mid) + nr3)), q2);
+    right = fma(fma(nr1, ar1, fma(-mid, ar2, nr3 * ar3)), frcp_weights(6.0 * ((nr1 + mid) + nr3)), q2);
   }
 }
 

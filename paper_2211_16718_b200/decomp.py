@@ -279,7 +279,8 @@ class DistHalo:
                 dist.all_reduce(red[0:3], op=dist.ReduceOp.MAX, group=halo.group)
                 dist.all_reduce(red[3:9], op=dist.ReduceOp.SUM, group=halo.group)
 
-        march = _DeviceMarch(plan, fields, gas, tparams, t0, stepper=stepper, reducer=reducer)
+        march = _DeviceMarch(plan, fields, gas, tparams, t0, stepper=stepper, reducer=reducer,
+                             global_points=spec.interior_points * self.layout.dims[2])
         return march.run(observer, dt_provider)
 
 

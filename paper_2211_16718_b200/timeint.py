@@ -252,7 +252,7 @@ class _Records:
         self.n += 1
 
 
-def _record(step: int, row: np.ndarray, spec: GridSpec, wall: float) -> StepRecord:
+def _record(step: int, row: np.ndarray, spec: GridSpec, wall: float, points: int) -> StepRecord:
     vol = spec.cell_volume()
     red = row[2:]
     return StepRecord(
@@ -262,7 +262,7 @@ def _record(step: int, row: np.ndarray, spec: GridSpec, wall: float) -> StepReco
         energy=float(red[_lib.HD_RED_ENERGY]) * vol,
         max_wavespeed=float(red[_lib.HD_RED_WAVESPEED]),
         wall_seconds=wall,
-        kinetic_energy=float(red[_lib.HD_RED_KE]) / spec.interior_points,
+        kinetic_energy=float(red[_lib.HD_RED_KE]) / points,
     )
 
 
@@ -294,9 +294,11 @@ class _DeviceMarch:
     """The fused single-device march shared by advance() and the decomposed driver."""
 
     def __init__(self, plan, fields: FieldSet, gas: GasModel, tparams: TimeParams, t0: float,
-                 stepper=None, reducer=None):
+                 stepper=None, reducer=None, global_points: int | None = None):
         self.plan = plan
         self.spec = fields.spec
+        # interior points of the whole (possibly decomposed) domain: the KE mean
+        self.points = global_points or fields.spec.interior_points
         self.gas = gas
         self.tp = tparams
         self.t0 = float(t0)
@@ -357,7 +359,7 @@ class _DeviceMarch:
                 self._check(step_base=0)
                 t = float(row[0])
                 wall = _time.perf_counter() - wall0
-                rec = _record(step, row, self.spec, wall)
+                rec = _record(step, row, self.spec, wall, self.points)
                 records.append(rec)
                 if observer is not None:
                     observer(rec)
@@ -366,7 +368,7 @@ class _DeviceMarch:
             self._check(step_base=0)
             total = _time.perf_counter() - last_wall
             per = total / max(step, 1)
-            records = [_record(s + 1, rows[s], self.spec, per) for s in range(step)]
+            records = [_record(s + 1, rows[s], self.spec, per, self.points) for s in range(step)]
             if step:
                 t = float(rows[step - 1][0])
         return AdvanceResult(fields=self.out, t=t, records=records)

@@ -267,7 +267,10 @@ def test_x_sweep_staged_matches_unstaged(hd, oracle, monkeypatch, mode):
         inc.data.fill_(0.25)
         hd.hyper_sweep(fs, 0, inc, mode=mode)
         outs.append(inc.numpy())
-    assert np.array_equal(outs[0], outs[1])
+    if mode == "exact":
+        assert np.array_equal(outs[0], outs[1])
+    else:  # different kernels may contract FMAs differently
+        assert _close(outs[1], outs[0], 1e-13)
     if mode == "exact":
         gz, gy, gx = P.shape
         g = 3
