@@ -44,13 +44,22 @@ extern "C" {
 #define HD_SCHEME_RK4 4
 
 /* stage parts (hd_stage_part): one RK stage, split around the halo seam.
- * Call in order; between LOCAL and HALO the z ghosts of the stage input must
- * arrive, between HALO and DIV the z ghosts of the viscous z-flux group. */
-#define HD_PART_LOCAL 1   /* x, y sweeps (fast: + viscous primitives): no z ghosts read */
-#define HD_PART_HALO 2    /* exact: z sweep + primitives; both: viscous fluxes */
-#define HD_PART_DIV 4     /* fast: viscous divergence added to the increment */
-#define HD_PART_UPDATE 8  /* fast: z sweep + RK update; exact: divergence + RK update */
+ * Call in this order; between LOCAL and PRIMS/HALO the z ghosts of the stage
+ * input must arrive, between MID and UPDATE the z ghosts of the viscous z-flux
+ * group (fields 5..8 of HD_BUF_VFLUX). */
+#define HD_PART_LOCAL 1   /* x sweep (exact: + y sweep): no z ghosts read */
+#define HD_PART_HALO 2    /* exact: z sweep + primitives; fast: exchanged-plane primitives;
+                             both: viscous fluxes */
+#define HD_PART_MID 4     /* fast: y sweep + D_x F_x + D_y F_y */
+#define HD_PART_UPDATE 8  /* fast: z sweep + D_z F_z + RK update + primitives of the new state;
+                             exact: viscous divergence + RK update */
 #define HD_PART_ALL 15
+#define HD_PART_PRIMS 16  /* fast: viscous primitives of the stage input (whole box); needed
+                             before HALO when the previous update did not produce them */
+
+/* hd_step flags */
+#define HD_STEP_PRIMS_VALID 1 /* HD_BUF_PRIM holds the primitives of u (the previous
+                                 hd_step on this plan ended with u): skip recomputing them */
 
 /* workspace buffers (hd_plan_buffer) */
 #define HD_BUF_STAGE 0 /* 10 fields: RK stage states, ping-pong halves (stage s writes half s%2) */
@@ -145,7 +154,7 @@ int hd_rhs(hd_plan* plan, double* u, double* inc, void* stream);
  * place, dt read from device memory.  Ghosts of u must be valid on entry and
  * are valid on exit (locally periodic axes).  `tag` identifies the step in
  * the error key. */
-int hd_step(hd_plan* plan, int scheme, double* u, const double* dt_dev, int64_t tag,
+int hd_step(hd_plan* plan, int scheme, double* u, const double* dt_dev, int64_t tag, int flags,
             void* stream);
 
 /* One part of one RK stage (decomposed runs).  Stage s reads u (s == 0) or

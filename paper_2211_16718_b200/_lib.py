@@ -21,7 +21,8 @@ HD_MODE_FAST = 0
 HD_MODE_EXACT = 1
 HD_SCHEME_RK3 = 3
 HD_SCHEME_RK4 = 4
-HD_PART_LOCAL, HD_PART_HALO, HD_PART_DIV, HD_PART_UPDATE, HD_PART_ALL = 1, 2, 4, 8, 15
+HD_PART_LOCAL, HD_PART_HALO, HD_PART_MID, HD_PART_UPDATE, HD_PART_ALL, HD_PART_PRIMS = 1, 2, 4, 8, 15, 16
+HD_STEP_PRIMS_VALID = 1
 (HD_BUF_STAGE, HD_BUF_ACC, HD_BUF_INC, HD_BUF_PRIM, HD_BUF_VFLUX, HD_BUF_RED, HD_BUF_CTX,
  HD_BUF_ERR) = range(8)
 (HD_RED_SIGNAL_MAX, HD_RED_SIGNAL_SUM, HD_RED_WAVESPEED, HD_RED_MASS, HD_RED_MOMX, HD_RED_MOMY,
@@ -100,7 +101,7 @@ def load(require_cuda: bool = False):
             "hd_parabolic_rhs": ([P, P, P, P], i32),
             "hd_central_diff4": ([P, P] + [i32] * 10 + [f64, P], i32),
             "hd_rhs": ([P, P, P, P], i32),
-            "hd_step": ([P, i32, P, P, i64, P], i32),
+            "hd_step": ([P, i32, P, P, i64, i32, P], i32),
             "hd_stage_part": ([P, i32, i32, i32, P, P, i64, P], i32),
             "hd_reduce_state": ([P, P, P, i64, P], i32),
             "hd_set_dt": ([P, P, i32, f64, f64, f64, P, i64, P], i32),

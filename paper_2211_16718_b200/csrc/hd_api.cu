@@ -235,13 +235,16 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   int rc = HD_OK;
   const bool exact = p->mode == HD_MODE_EXACT;
   double* prim = visc ? buf(p, HD_BUF_PRIM) : nullptr;
-  // LOCAL: x and y sweeps (fast: the y sweep also stores the viscous primitives).
-  // Neither reads z ghosts, so a z-halo exchange of `us` can be in flight.
+  double* vflux = visc ? buf(p, HD_BUF_VFLUX) : nullptr;
+  const bool zx = !p->geo.periodic[2];  // z ghosts come from a halo exchange
+  // LOCAL: sweeps that read no z ghosts (a z-halo exchange of `us` can be in flight)
   if (parts & HD_PART_LOCAL) {
     rc = launch_sweep(p, 0, us, inc, 0, 1, t, s);
-    if (!rc) rc = exact ? launch_sweep(p, 1, us, inc, 1, 0, t, s)
-                        : launch_sweep_prims(p, us, inc, prim, t, s);
+    if (!rc && exact) rc = launch_sweep(p, 1, us, inc, 1, 0, t, s);
   }
+  // PRIMS (fast): viscous primitives of the stage input over the whole box;
+  // otherwise they come from the previous stage's update kernel
+  if (!rc && (parts & HD_PART_PRIMS) && !exact && visc) rc = launch_prims(p, us, s);
   // HALO (reads the z ghosts of `us`)
   //   exact: z sweep, primitives of the whole box, viscous fluxes
   //   fast:  primitives of exchanged ghost planes, viscous fluxes
@@ -249,27 +252,28 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
     if (exact) {
       rc = launch_sweep(p, 2, us, inc, 1, 0, t, s);
       if (!rc && visc) rc = launch_prims(p, us, s);
-    } else if (visc && !p->geo.periodic[2]) {
+    } else if (visc && zx) {
       const int g = p->geo.g, nz = p->geo.n[2];
       rc = launch_prims_planes(p, us, 0, g, s);
       if (!rc) rc = launch_prims_planes(p, us, nz + g, nz + 2 * g, s);
     }
     if (!rc && visc) rc = launch_gradflux(p, s);
   }
-  // DIV (reads the z ghosts of the viscous z-flux group) -- fast: inc += div F
-  if (!rc && (parts & HD_PART_DIV) && !exact && visc)
-    rc = launch_divergence(p, 7, inc, inc, 0, scheme, stage, nullptr, nullptr, s);
-  // UPDATE: RK stage update (exact: after the viscous divergence, viscous.py:112-120
-  // order; fast: fused into the z sweep, the divergence having been added by DIV)
+  // MID (fast): y sweep + D_x F_x + D_y F_y (no z ghosts of the fluxes read)
+  if (!rc && (parts & HD_PART_MID) && !exact) rc = launch_sweep_visc(p, us, inc, vflux, t, s);
+  // UPDATE (reads the z ghosts of the viscous z-flux group)
+  //   exact: divergence in the viscous.py:112-120 order + RK update
+  //   fast:  z sweep + D_z F_z + RK update + primitives of the new state
   if (!rc && (parts & HD_PART_UPDATE)) {
     if (!dt_dev) return HD_E_ARG;
     rc = exact ? launch_divergence(p, visc ? 7 : 0, inc, nullptr, 1, scheme, stage, u, dt_dev, s)
-               : launch_sweep_update(p, us, inc, scheme, stage, u, dt_dev, t, s);
+               : launch_sweep_update(p, us, inc, vflux, prim, scheme, stage, u, dt_dev, t, s);
   }
   return rc;
 }
 
-int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag, void* stream) {
+int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag, int flags,
+            void* stream) {
   if (!p || !u || !dt_dev) return HD_E_ARG;
   if (!p->ws) return HD_E_WORKSPACE;
   if (scheme != HD_SCHEME_RK3 && scheme != HD_SCHEME_RK4) return HD_E_ARG;
@@ -277,8 +281,11 @@ int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag
     if (!p->geo.periodic[d]) return HD_E_UNSUPPORTED;  // decomposed runs use hd_stage_part
   // timeint.py:153: the rhs syncs the ghosts of its input first
   int rc = launch_fill_ghosts(p, u, 5, 7, S(stream));
-  for (int st = 0; st < nstages(scheme) && !rc; ++st)
-    rc = hd_stage_part(p, scheme, st, HD_PART_ALL, u, dt_dev, tag, stream);
+  for (int st = 0; st < nstages(scheme) && !rc; ++st) {
+    int parts = HD_PART_ALL;
+    if (st == 0 && !(flags & HD_STEP_PRIMS_VALID)) parts |= HD_PART_PRIMS;
+    rc = hd_stage_part(p, scheme, st, parts, u, dt_dev, tag, stream);
+  }
   return rc;
 }
 

@@ -176,7 +176,7 @@ __device__ __forceinline__ void rk_store(const RKArgs& r, const Geo& G, int i, i
 // fast-mode RK update with the base state and accumulator already in registers
 __device__ __forceinline__ void rk_store_pre(const RKArgs& r, const Geo& G, int i, int j, int k,
                                              const double (&kv)[NV], const double (&u0)[NV],
-                                             const double (&acc)[NV]) {
+                                             const double (&acc)[NV], double (&outv)[NV]) {
   const double dt = *r.dt;
   const int64_t q = G.idx(i, j, k);
   const int pm = periodic_mask(G);
@@ -189,6 +189,7 @@ __device__ __forceinline__ void rk_store_pre(const RKArgs& r, const Geo& G, int 
     if (r.rd_us) out = fma(r.a1, r.stage_in[off], out);
     if (r.wr_acc) r.acc[off] = fma(r.b0, acc[v], r.b1 * kv[v]);
     store_face_images(dst + v * G.npts, G, i, j, k, pm, out);
+    outv[v] = out;
   }
 }
 
@@ -210,6 +211,29 @@ __device__ __forceinline__ void add_viscous_divergence(const double* __restrict_
       const double dv = cd4<EXACT>(vf + (int64_t)vf_field(d, row) * np + q, st, coef);
       if constexpr (EXACT) kv[row] = xa(kv[row], dv);
       else kv[row] += dv;
+    }
+  }
+}
+
+// L1 prefetch of every operand add_viscous_divergence reads at point q
+__device__ __forceinline__ void prefetch_divergence(const double* vf, const Geo& G, int64_t q,
+                                                    int dmask) {
+  const int64_t np = G.npts;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (!(dmask & (1 << d))) continue;
+    const int64_t st = G.stride(d);
+#pragma unroll
+    for (int row = 1; row < NV; ++row) {
+      const double* f = vf + (int64_t)vf_field(d, row) * np + q;
+      if (d == 0) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(f - 2));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(f + 2));
+      } else {
+#pragma unroll
+        for (int o = -2; o <= 2; ++o)
+          if (o) asm volatile("prefetch.global.L1 [%0];" ::"l"(f + o * st));
+      }
     }
   }
 }

@@ -111,11 +111,13 @@ void count_launches(int n);
 // launchers implemented in the .cu files
 int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int accumulate,
                  int check, int64_t tag, cudaStream_t s);
-// fused stage pipeline (fast mode): y sweep + viscous primitives; z sweep + RK update
-int launch_sweep_prims(const hd_plan* p, const double* u, double* inc, double* prim, int64_t tag,
-                       cudaStream_t s);
-int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, int scheme, int stage,
-                        double* u, const double* dt_dev, int64_t tag, cudaStream_t s);
+// fused stage pipeline (fast mode): y sweep + x/y viscous divergence; z sweep +
+// z viscous divergence + RK update + primitives of the new stage state
+int launch_sweep_visc(const hd_plan* p, const double* u, double* inc, const double* vflux,
+                      int64_t tag, cudaStream_t s);
+int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, const double* vflux,
+                        double* prim, int scheme, int stage, double* u, const double* dt_dev,
+                        int64_t tag, cudaStream_t s);
 int launch_prims_planes(const hd_plan* p, const double* u, int z_lo, int z_hi, cudaStream_t s);
 int launch_fill_ghosts(const hd_plan* p, double* f, int nfields, int axis_mask, cudaStream_t s);
 int launch_prims(const hd_plan* p, const double* u, cudaStream_t s);

@@ -303,20 +303,25 @@ constexpr int SWEEP_THREADS = 64;
 #ifndef HD_SWEEP_MIN_BLOCKS_X
 #define HD_SWEEP_MIN_BLOCKS_X 4
 #endif
+#ifndef HD_SWEEP_FLUX_WINDOW
+#define HD_SWEEP_FLUX_WINDOW 0
+#endif
 template <int DIM> struct SweepCfg {
   static constexpr bool smem_window = DIM != 0 && HD_SWEEP_SMEM_WINDOW_YZ;
   static constexpr int min_blocks = DIM == 0 ? HD_SWEEP_MIN_BLOCKS_X : HD_SWEEP_MIN_BLOCKS_YZ;
 };
 
-// What a sweep does besides -dF/dx (the fused stage pipeline, hd_api.cu):
+// What a sweep does besides -dF/dx (the fast-mode stage pipeline, hd_api.cu):
 //   ROLE_PLAIN  inc (-)= dF/dx
-//   ROLE_PRIMS  y sweep: also stores the viscous primitives (u, v, w, T) of the
-//               points it owns (coalesced: lanes are consecutive x), plus their face
-//               images along locally periodic axes
-//   ROLE_UPDATE z sweep (fast mode, last kernel of a stage): the finished
-//               increment (viscous divergence already added) feeds the RK stage
-//               update (timeint.py:168-193) instead of being stored
-constexpr int ROLE_PLAIN = 0, ROLE_PRIMS = 1, ROLE_UPDATE = 2;
+//   ROLE_VISC   y sweep: also adds the x and y viscous flux divergence
+//               D_x F_x + D_y F_y (viscous.py:119-120) of the cell it writes
+//   ROLE_UPDATE z sweep, last kernel of a stage: adds D_z F_z, feeds the finished
+//               increment to the RK stage update (timeint.py:168-193) instead of
+//               storing it, and stores the viscous primitives (u, v, w, T) of the
+//               new stage state (with face images) for the next stage's fluxes
+// The stencil operands of the divergence are pulled into L1 at the top of the
+// iteration that consumes them (prefetch.global.L1: no registers held).
+constexpr int ROLE_PLAIN = 0, ROLE_VISC = 1, ROLE_UPDATE = 2;
 
 struct SweepArgs {
   Geo geo;
@@ -329,9 +334,10 @@ struct SweepArgs {
   int check;        // latch positivity of interior points
   unsigned long long* err;
   int64_t tag;
-  // ROLE_PRIMS
-  double* prim;
+  // ROLE_VISC / ROLE_UPDATE
+  const double* vflux;  // 9 symmetric viscous flux fields (nullptr: inviscid)
   // ROLE_UPDATE
+  double* prim;         // primitives of the new stage state (nullptr: not needed)
   RKArgs rk;
 };
 
@@ -390,10 +396,33 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   // consecutive threads hold consecutive doubles, so every access is bank-
   // conflict free, and the 45-double window stays out of the register file.
   // Otherwise a register window: point w holds line position c - 2 + w.
-  __shared__ double ring[SMEM_WINDOW ? 5 * 9 * SWEEP_THREADS : 1];
+  // The VISC/UPDATE roles append 4 columns: the viscous flux group F_dim
+  // (differentiated along the sweep) at the same positions, so D_dim F_dim
+  // reads each flux value from HBM once.
+  // (HD_SWEEP_FLUX_WINDOW, off by default: measured slower at 512^3 -- the
+  // larger ring leaves too little L1 for the other streams of the kernel;
+  // the default reads the stencil directly, operands prefetched into L1.)
+  constexpr bool VROLE = ROLE != ROLE_PLAIN;
+  constexpr bool FWIN = VROLE && HD_SWEEP_FLUX_WINDOW;
+  constexpr int RV = FWIN ? 13 : 9;  // values per ring slot
+  __shared__ double ring[SMEM_WINDOW ? 5 * RV * SWEEP_THREADS : 1];
   double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
-  auto slot = [&](int m) -> double* { return mine + ((m + 5) % 5) * (9 * SWEEP_THREADS); };
+  auto slot = [&](int m) -> double* { return mine + ((m + 5) % 5) * (RV * SWEEP_THREADS); };
   double wu[5][NV], wf[5][NV];
+  // viscous flux window: position p -> slot(p) columns 9..12; F(c+1) enters at
+  // iteration c from fpre (loaded one iteration earlier)
+  const bool fwin = FWIN && SMEM_WINDOW && a.vflux;
+  double fpre[4];
+  auto ffetch = [&](int m) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      fpre[r] = __ldg(a.vflux + (int64_t)vf_field(DIM, r + 1) * np + base + (int64_t)m * sd);
+  };
+  auto fstore = [&](int m) {
+    double* sp = slot(m) + 9 * SWEEP_THREADS;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) sp[r * SWEEP_THREADS] = fpre[r];
+  };
 
   // raw loads are issued one iteration before the point enters the window
   // (and the inc read of a cell at the top of the iteration that writes it),
@@ -419,14 +448,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
       if (!(uu[0] > 0.0)) latch_error(a.err, a.tag, 1, base + (int64_t)m * sd);
       else if (!(pv[3] > 0.0)) latch_error(a.err, a.tag, 2, base + (int64_t)m * sd);
     }
-    if constexpr (ROLE == ROLE_PRIMS) {
-      if (a.prim && m >= c0 && m < c1) {
-        // viscous.py:80-81: T = gamma p / rho
-        if constexpr (EXACT) pv[3] = xd(xm(a.ph.gamma, pv[3]), uu[0]);
-        else pv[3] = a.ph.gamma * pv[3] * inv;
-        store_prim(a.prim, G, DIM == 0 ? m : li, DIM == 1 ? m : lj, DIM == 2 ? m : lk, pv);
-      }
-    }
   };
 
   double pre[NV];
@@ -436,6 +457,13 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
     ingest(c0 - 3 + w, pre, wu[w + 1], wf[w + 1]);
   }
   fetch(c0 + 1, pre);
+  if (fwin) {
+    for (int m = c0 - 3; m < c0; ++m) {
+      ffetch(m);
+      fstore(m);
+    }
+    ffetch(c0);
+  }
 
   double lu[NV], lf[NV];  // left states at c-1/2 (carried)
   double fprev[NV];
@@ -453,8 +481,16 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
     }
     ingest(c + 2, pre, wu[4], wf[4]);
     if (c < c1) fetch(c + 3, pre);
+    if (fwin) {
+      fstore(c + 1);
+      if (c < c1) ffetch(c + 2);
+    }
     const bool wr = c > c0;
     double* q = inc + (int64_t)(c - 1) * sd;
+    if constexpr (VROLE && !FWIN) {
+      if (wr && a.vflux)
+        prefetch_divergence(a.vflux, G, base + (int64_t)(c - 1) * sd, ROLE == ROLE_VISC ? 3 : 4);
+    }
     // ROLE_UPDATE: the RK inputs of cell c-1 (base state, accumulator) are
     // loaded here, a full window of FP64 work before the update consumes them
     double ru0[NV], racc[NV];
@@ -506,12 +542,44 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
           if constexpr (EXACT) val[v] = xs(old[v], xm(xs(flux[v], fprev[v]), a.inv_dx));
           else val[v] = old[v] - (flux[v] - fprev[v]) * a.inv_dx;
         }
-        if constexpr (ROLE == ROLE_UPDATE) {
+        if (fwin) {
+          // y sweep: D_x F_x from row loads (x neighbours share the lanes' lines);
+          // then D_dim F_dim from the window, positions c-3 .. c+1
+          if constexpr (ROLE == ROLE_VISC)
+            add_viscous_divergence<EXACT>(a.vflux, G, base + (int64_t)(c - 1) * sd, 1, val);
+          const double* m2 = slot(c - 3) + 9 * SWEEP_THREADS;
+          const double* m1 = slot(c - 2) + 9 * SWEEP_THREADS;
+          const double* p1 = slot(c) + 9 * SWEEP_THREADS;
+          const double* p2 = slot(c + 1) + 9 * SWEEP_THREADS;
+          const double coef = 1.0 / (12.0 * G.h[DIM]);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int o = r * SWEEP_THREADS;
+            val[r + 1] += (8.0 * (p1[o] - m1[o]) + (m2[o] - p2[o])) * coef;
+          }
+        } else if (VROLE && a.vflux) {  // direct stencil loads (L1-prefetched above)
+          add_viscous_divergence<EXACT>(a.vflux, G, base + (int64_t)(c - 1) * sd,
+                                        ROLE == ROLE_VISC ? 3 : 4, val);
+        }
+        if constexpr (ROLE == ROLE_VISC) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) q[v * np] = val[v];
+        } else if constexpr (ROLE == ROLE_UPDATE) {
           int ci = li, cj = lj, ck = lk;
           if (DIM == 0) ci = c - 1;
           else if (DIM == 1) cj = c - 1;
           else ck = c - 1;
-          rk_store_pre(a.rk, G, ci, cj, ck, val, ru0, racc);
+          double out[NV];
+          rk_store_pre(a.rk, G, ci, cj, ck, val, ru0, racc, out);
+          if (a.prim) {
+            // viscous.py:80-81 primitives of the new state (u, v, w, T = gamma p / rho)
+            const double inv = frcp(out[0]);
+            double pv[4] = {out[1] * inv, out[2] * inv, out[3] * inv, 0.0};
+            const double p = gm1 * (out[4] - (0.5 * inv) * (out[1] * out[1] + out[2] * out[2] +
+                                                            out[3] * out[3]));
+            pv[3] = a.ph.gamma * p * inv;
+            store_prim(a.prim, G, ci, cj, ck, pv);
+          }
         } else {
 #pragma unroll
           for (int v = 0; v < NV; ++v) q[v * np] = val[v];
@@ -748,19 +816,22 @@ int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int ac
   }
 }
 
-int launch_sweep_prims(const hd_plan* p, const double* u, double* inc, double* prim, int64_t tag,
-                       cudaStream_t s) {
+int launch_sweep_visc(const hd_plan* p, const double* u, double* inc, const double* vflux,
+                      int64_t tag, cudaStream_t s) {
   int nseg;
   SweepArgs a = make_args(p, 1, u, inc, 1, 0, tag, nseg);
-  a.prim = prim;
+  a.vflux = vflux;
   if (p->mode == HD_MODE_EXACT) return HD_E_UNSUPPORTED;  // exact mode runs the unfused stage
-  return launch_dim<1, false, ROLE_PRIMS>(p, a, nseg, s);
+  return launch_dim<1, false, ROLE_VISC>(p, a, nseg, s);
 }
 
-int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, int scheme, int stage,
-                        double* u, const double* dt_dev, int64_t tag, cudaStream_t s) {
+int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, const double* vflux,
+                        double* prim, int scheme, int stage, double* u, const double* dt_dev,
+                        int64_t tag, cudaStream_t s) {
   int nseg;
   SweepArgs a = make_args(p, 2, u_stage, inc, 1, 0, tag, nseg);
+  a.vflux = vflux;
+  a.prim = prim;
   a.rk = make_rk(p, scheme, stage, u, dt_dev);
   if (p->mode == HD_MODE_EXACT) return HD_E_UNSUPPORTED;  // exact mode runs the unfused stage
   return launch_dim<2, false, ROLE_UPDATE>(p, a, nseg, s);

@@ -13,7 +13,8 @@ replaced by torch.distributed over NCCL/NVLink:
   overlaps the x and y sweeps, which never read z ghosts; the z sweep waits
   on it (``hd_stage_part`` HD_PART_LOCAL / HD_PART_HALO);
 * the viscous flux faces of the z-differentiated flux group (4 of the 9
-  symmetric flux fields, g planes) are exchanged before the divergence;
+  symmetric flux fields, g planes) are exchanged while the y sweep runs, before
+  the z sweep that differentiates them;
 * the CFL signal and diagnostics are combined with ``all_reduce`` (MAX for
   signals, SUM for totals) on device tensors -- dt never leaves HBM.
 
@@ -266,13 +267,17 @@ class DistHalo:
             plan.fill_ghosts(u, NVARS)  # x/y wrap of the step input (z: exchanged below)
             for s in range(nst):
                 us = u if s == 0 else stage_buf[((s - 1) % 2) * half: ((s - 1) % 2 + 1) * half]
-                works = halo.exchange_z_async(us, NVARS, spec)   # overlaps the x/y sweeps
+                works = halo.exchange_z_async(us, NVARS, spec)   # overlaps the x sweep
                 plan.stage_part(scheme, s, _lib.HD_PART_LOCAL, u, dt_dev, tag)
                 halo.wait(works)
-                plan.stage_part(scheme, s, _lib.HD_PART_HALO, u, dt_dev, tag)
-                if visc:
-                    halo.wait(halo.exchange_z_async(vflux_z, 4, spec))
-                plan.stage_part(scheme, s, _lib.HD_PART_DIV | _lib.HD_PART_UPDATE, u, dt_dev, tag)
+                parts = _lib.HD_PART_HALO
+                if s == 0 and tag == 0:  # primitives of u not yet produced by an update
+                    parts |= _lib.HD_PART_PRIMS
+                plan.stage_part(scheme, s, parts, u, dt_dev, tag)
+                works = halo.exchange_z_async(vflux_z, 4, spec) if visc else []
+                plan.stage_part(scheme, s, _lib.HD_PART_MID, u, dt_dev, tag)  # overlaps it
+                halo.wait(works)
+                plan.stage_part(scheme, s, _lib.HD_PART_UPDATE, u, dt_dev, tag)
 
         def reducer(red):
             if halo.layout.dims[2] > 1:

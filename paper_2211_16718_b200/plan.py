@@ -140,8 +140,8 @@ class Plan:
     def rhs(self, u, inc) -> None:
         _lib.check(self.L.hd_rhs(self.h, _ptr(u), _ptr(inc), _stream_ptr()), "hd_rhs")
 
-    def step(self, scheme: int, u, dt_dev, tag: int) -> None:
-        _lib.check(self.L.hd_step(self.h, scheme, _ptr(u), _ptr(dt_dev), tag, _stream_ptr()),
+    def step(self, scheme: int, u, dt_dev, tag: int, flags: int = 0) -> None:
+        _lib.check(self.L.hd_step(self.h, scheme, _ptr(u), _ptr(dt_dev), tag, flags, _stream_ptr()),
                    "hd_step")
 
     def stage_part(self, scheme: int, stage: int, parts: int, u, dt_dev, tag: int) -> None:

@@ -16,11 +16,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=512)
 ap.add_argument("--mode", default="fast")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--mu", type=float, default=0.006)
 a = ap.parse_args()
 hd.set_mode(a.mode)
 spec = hd.GridSpec((a.n,) * 3)
 ic = hd.make_initial_condition(spec, hd.HitParams(), backend="torch" if a.n > 128 else "numpy")
-gas = hd.GasModel(mu=0.006)
+gas = hd.GasModel(mu=a.mu)
 plan = hd.get_plan(spec, gas)
 hd.fill_ghosts_periodic(ic)
 inc = plan.fields(hd._lib.HD_BUF_INC, 5)
