@@ -251,8 +251,9 @@ class DistHalo:
     def advance(self, fields: FieldSet, gas: GasModel, tparams, weno_params: WenoParams,
                 delta: float, t0: float, observer, dt_provider, mode):
         from .plan import get_plan
-        from .timeint import _DeviceMarch, _SCHEME_CODE
+        from .timeint import _SCHEME_CODE, _as_device, _DeviceMarch
 
+        fields = _as_device(fields)  # host (pinned) buffers are uploaded once
         spec = fields.spec
         plan = get_plan(spec, gas, weno_params, delta, mode, periodic=self.periodic)
         scheme = _SCHEME_CODE[tparams.scheme]
