@@ -14,6 +14,13 @@ __device__ __forceinline__ double cd4(const double* __restrict__ s, int64_t st, 
   return (8.0 * (p1 - m1) + (m2 - p2)) * coef;
 }
 
+// the same stencil on values already in registers / shared memory
+template <bool EXACT>
+__device__ __forceinline__ double cd4v(double m2, double m1, double p1, double p2, double coef) {
+  if constexpr (EXACT) return xm(xa(xs(xa(-p2, xm(8.0, p1)), xm(8.0, m1)), m2), coef);
+  return (8.0 * (p1 - m1) + (m2 - p2)) * coef;
+}
+
 // Writes v at interior point (i,j,k) of field f and at its periodic images
 // along the axes in `mask` (only those that wrap locally).
 __device__ __forceinline__ void store_with_images(double* f, const Geo& G, int i, int j, int k,

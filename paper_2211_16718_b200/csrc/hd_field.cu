@@ -9,6 +9,8 @@
 //   rk_update_kernel     timeint.py:168-193 when mu == 0 (viscous.py:72-73 short-circuit)
 //   central_diff4_kernel kernels.py:207-227 (stand-alone, for the operator API)
 //   reduce kernels       timeint.py:100-131 (CFL signal, totals, max wavespeed, KE)
+#include <cstdlib>
+
 #include "hd_device.cuh"
 
 namespace hd {
@@ -126,28 +128,11 @@ int launch_prims_planes(const hd_plan* p, const double* u, int z_lo, int z_hi, c
 // viscous fluxes: 12 gradients -> tau, heat flux -> F_d = (tau_0d, tau_1d, tau_2d, work_d),
 // stored symmetrically as 9 fields (hd_device.cuh VF_*)
 // ---------------------------------------------------------------------------
+// viscous.py:92-116 at one point: stress, heat flux, the 9 symmetric flux values
 template <bool EXACT>
-__global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict__ prim,
-                                                       double* __restrict__ vf, Geo G, double mu,
-                                                       double q_coef) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  const int k = blockIdx.z;
-  if (i >= G.n[0] || j >= G.n[1]) return;
-  const int64_t np = G.npts;
-  const int64_t q = G.idx(i, j, k);
-  const int64_t st[3] = {1, G.sy, G.sz};
-  double coef[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) coef[d] = 1.0 / (12.0 * G.h[d]);
-  double gr[3][3], gT[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int d = 0; d < 3; ++d) gr[a][d] = cd4<EXACT>(prim + a * np + q, st[d], coef[d]);
-#pragma unroll
-  for (int d = 0; d < 3; ++d) gT[d] = cd4<EXACT>(prim + 3 * np + q, st[d], coef[d]);
-  const double vel[3] = {__ldg(prim + q), __ldg(prim + np + q), __ldg(prim + 2 * np + q)};
+__device__ __forceinline__ void viscous_flux_point(const double (&gr)[3][3], const double (&gT)[3],
+                                                   const double (&vel)[3], double mu, double q_coef,
+                                                   double (&val)[VF_N]) {
   double tau[3][3];
   if constexpr (EXACT) {
     const double div = xa(xa(gr[0][0], gr[1][1]), gr[2][2]);
@@ -176,13 +161,149 @@ __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict_
       w[d] = vel[0] * tau[0][d] + vel[1] * tau[1][d] + vel[2] * tau[2][d] - q_coef * gT[d];
     }
   }
-  const double val[VF_N] = {tau[0][0], tau[0][1], tau[1][1], w[0], w[1],
-                            tau[0][2], tau[1][2], tau[2][2], w[2]};
+  val[0] = tau[0][0];
+  val[1] = tau[0][1];
+  val[2] = tau[1][1];
+  val[3] = w[0];
+  val[4] = w[1];
+  val[5] = tau[0][2];
+  val[6] = tau[1][2];
+  val[7] = tau[2][2];
+  val[8] = w[2];
+}
+
+template <bool EXACT>
+__global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict__ prim,
+                                                       double* __restrict__ vf, Geo G, double mu,
+                                                       double q_coef) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = blockIdx.z;
+  if (i >= G.n[0] || j >= G.n[1]) return;
+  const int64_t np = G.npts;
+  const int64_t q = G.idx(i, j, k);
+  const int64_t st[3] = {1, G.sy, G.sz};
+  double coef[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) coef[d] = 1.0 / (12.0 * G.h[d]);
+  double gr[3][3], gT[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) gr[a][d] = cd4<EXACT>(prim + a * np + q, st[d], coef[d]);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) gT[d] = cd4<EXACT>(prim + 3 * np + q, st[d], coef[d]);
+  const double vel[3] = {__ldg(prim + q), __ldg(prim + np + q), __ldg(prim + 2 * np + q)};
+  double val[VF_N];
+  viscous_flux_point<EXACT>(gr, gT, vel, mu, q_coef, val);
   const int pm = periodic_mask(G);
 #pragma unroll
   for (int f = 0; f < VF_N; ++f)
     store_face_images(vf + (int64_t)f * np, G, i, j, k, pm & vf_axes(f), val[f]);
 }
+
+// gradflux with z marching (blocks of 32 x 8 columns): the z stencil comes from
+// a per-thread register queue of 5 planes (each prims value is loaded once per
+// column), the x/y stencils from a shared-memory plane tile with a 2-point halo.
+// Needs n_x % 32 == 0 and n_y % 8 == 0 (else gradflux_kernel).
+constexpr int GZ_TX = 32, GZ_TY = 8, GZ_H = 2;
+constexpr int GZ_PX = GZ_TX + 2 * GZ_H, GZ_PY = GZ_TY + 2 * GZ_H;
+
+template <bool EXACT>
+__global__ void __launch_bounds__(GZ_TX * GZ_TY, 2) gradflux_zm_kernel(
+    const double* __restrict__ prim, double* __restrict__ vf, Geo G, double mu, double q_coef,
+    int zseg) {
+  // two plane tiles (double-buffered: one barrier per plane); every load is
+  // issued one plane before it is needed (z queue: plane k+3; ring: plane k+1)
+  __shared__ double tile[2][4][GZ_PY][GZ_PX];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int i = blockIdx.x * GZ_TX + tx, j = blockIdx.y * GZ_TY + ty;
+  const int k0 = blockIdx.z * zseg;
+  const int k1 = min(k0 + zseg, G.n[2]);
+  const int64_t np = G.npts;
+  const int64_t sz = G.sz;
+  double coef[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) coef[d] = 1.0 / (12.0 * G.h[d]);
+  // z queue: qz[f][w] = prims field f at plane k - 2 + w of this column
+  double qz[4][5], nq[4];
+  const int64_t col = G.idx(i, j, 0);
+#pragma unroll
+  for (int w = 1; w < 5; ++w)
+#pragma unroll
+    for (int f = 0; f < 4; ++f) qz[f][w] = __ldg(prim + f * np + col + (int64_t)(k0 - 3 + w) * sz);
+#pragma unroll
+  for (int f = 0; f < 4; ++f) nq[f] = __ldg(prim + f * np + col + (int64_t)(k0 + 2) * sz);
+  // halo ring of the plane tile (minus the never-read corners): <= 1 point per thread
+  const int r = ty * GZ_TX + tx;
+  int px = 0, py = 0;
+  bool has_ring = r < GZ_PX * GZ_PY - GZ_TX * GZ_TY;
+  if (has_ring) {  // ring index -> (px, py): rows above/below the tile, then side columns
+    if (r < 2 * GZ_H * GZ_PX) {
+      py = r / GZ_PX;
+      px = r % GZ_PX;
+      if (py >= GZ_H) py += GZ_TY;
+    } else {
+      const int s = r - 2 * GZ_H * GZ_PX;
+      py = GZ_H + s / (2 * GZ_H);
+      px = s % (2 * GZ_H);
+      if (px >= GZ_H) px += GZ_TX;
+    }
+    has_ring = !((px < GZ_H || px >= GZ_H + GZ_TX) && (py < GZ_H || py >= GZ_H + GZ_TY));
+  }
+  const int64_t rcol = G.idx(blockIdx.x * GZ_TX + px - GZ_H, blockIdx.y * GZ_TY + py - GZ_H, 0);
+  double rv[4];
+  if (has_ring)
+#pragma unroll
+    for (int f = 0; f < 4; ++f) rv[f] = __ldg(prim + f * np + rcol + (int64_t)k0 * sz);
+  for (int k = k0; k < k1; ++k) {
+    const int b = k & 1;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) qz[f][w] = qz[f][w + 1];
+      qz[f][4] = nq[f];
+      tile[b][f][ty + GZ_H][tx + GZ_H] = qz[f][2];
+      if (has_ring) tile[b][f][py][px] = rv[f];
+    }
+    if (k + 1 < k1) {
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        nq[f] = __ldg(prim + f * np + col + (int64_t)(k + 3) * sz);
+        if (has_ring) rv[f] = __ldg(prim + f * np + rcol + (int64_t)(k + 1) * sz);
+      }
+    }
+    __syncthreads();
+    double gr[3][3], gT[3];
+    const int cx = tx + GZ_H, cy = ty + GZ_H;
+    double (*tl)[GZ_PY][GZ_PX] = tile[b];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const double gx = cd4v<EXACT>(tl[f][cy][cx - 2], tl[f][cy][cx - 1], tl[f][cy][cx + 1],
+                                     tl[f][cy][cx + 2], coef[0]);
+      const double gy = cd4v<EXACT>(tl[f][cy - 2][cx], tl[f][cy - 1][cx], tl[f][cy + 1][cx],
+                                     tl[f][cy + 2][cx], coef[1]);
+      const double gz = cd4v<EXACT>(qz[f][0], qz[f][1], qz[f][3], qz[f][4], coef[2]);
+      if (f < 3) {
+        gr[f][0] = gx;
+        gr[f][1] = gy;
+        gr[f][2] = gz;
+      } else {
+        gT[0] = gx;
+        gT[1] = gy;
+        gT[2] = gz;
+      }
+    }
+    const double vel[3] = {qz[0][2], qz[1][2], qz[2][2]};
+    double val[VF_N];
+    viscous_flux_point<EXACT>(gr, gT, vel, mu, q_coef, val);
+    const int pm = periodic_mask(G);
+#pragma unroll
+    for (int f = 0; f < VF_N; ++f)
+      store_face_images(vf + (int64_t)f * np, G, i, j, k, pm & vf_axes(f), val[f]);
+  }
+}
+
 
 int launch_gradflux(const hd_plan* p, cudaStream_t s) {
   const Geo& G = p->geo;
@@ -190,6 +311,21 @@ int launch_gradflux(const hd_plan* p, cudaStream_t s) {
   double* vf = (double*)(p->ws + p->off[HD_BUF_VFLUX]);
   const double mu = p->phys.mu;
   const double q_coef = (-mu) / ((p->phys.gamma - 1.0) * p->phys.prandtl);  // viscous.py:107
+  if (G.n[0] % GZ_TX == 0 && G.n[1] % GZ_TY == 0 && !getenv("HD_NO_GZ")) {
+    // z segments: enough blocks for ~4 waves of 2 blocks per SM
+    const int64_t cols = (int64_t)(G.n[0] / GZ_TX) * (G.n[1] / GZ_TY);
+    int nseg = (int)((p->sm_count * 2 * 4 + cols - 1) / cols);
+    nseg = nseg < 1 ? 1 : (nseg > G.n[2] ? G.n[2] : nseg);
+    const int zseg = (G.n[2] + nseg - 1) / nseg;
+    nseg = (G.n[2] + zseg - 1) / zseg;
+    dim3 block(GZ_TX, GZ_TY, 1), grid(G.n[0] / GZ_TX, G.n[1] / GZ_TY, nseg);
+    if (p->mode == HD_MODE_EXACT)
+      gradflux_zm_kernel<true><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg);
+    else
+      gradflux_zm_kernel<false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg);
+    hd::count_launches(1);
+    return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+  }
   dim3 block(32, 4, 1), grid((G.n[0] + 31) / 32, (G.n[1] + 3) / 4, G.n[2]);
   if (p->mode == HD_MODE_EXACT)
     gradflux_kernel<true><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef);
