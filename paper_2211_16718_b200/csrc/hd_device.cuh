@@ -181,12 +181,43 @@ __device__ __forceinline__ void rk_store(const RKArgs& r, const Geo& G, int i, i
 }
 
 // fast-mode RK update with the base state and accumulator already in registers
+// Index deltas of the face images of interior point (i,j,k) along the axes in
+// `mask` (at most one per axis once n >= 2g); returns how many.
+__device__ __forceinline__ int face_image_deltas(const Geo& G, int i, int j, int k, int mask,
+                                                 int64_t (&dl)[3]) {
+  int nd = 0;
+  const int g = G.g;
+  if (mask & 1) {
+    if (i < g) dl[nd++] = G.n[0];
+    else if (i >= G.n[0] - g) dl[nd++] = -(int64_t)G.n[0];
+  }
+  if (mask & 2) {
+    if (j < g) dl[nd++] = (int64_t)G.n[1] * G.sy;
+    else if (j >= G.n[1] - g) dl[nd++] = -(int64_t)G.n[1] * G.sy;
+  }
+  if (mask & 4) {
+    if (k < g) dl[nd++] = (int64_t)G.n[2] * G.sz;
+    else if (k >= G.n[2] - g) dl[nd++] = -(int64_t)G.n[2] * G.sz;
+  }
+  return nd;
+}
+
+// N fields (stride npts) at flat point q and its face images
+template <int N>
+__device__ __forceinline__ void store_point_images(double* f, int64_t np, int64_t q, int nd,
+                                                   const int64_t (&dl)[3], const double (&v)[N]) {
+#pragma unroll
+  for (int c = 0; c < N; ++c) f[q + c * np] = v[c];
+  for (int t = 0; t < nd; ++t)
+#pragma unroll
+    for (int c = 0; c < N; ++c) f[q + dl[t] + c * np] = v[c];
+}
+
 __device__ __forceinline__ void rk_store_pre(const RKArgs& r, const Geo& G, int i, int j, int k,
                                              const double (&kv)[NV], const double (&u0)[NV],
                                              const double (&acc)[NV], double (&outv)[NV]) {
   const double dt = *r.dt;
   const int64_t q = G.idx(i, j, k);
-  const int pm = periodic_mask(G);
   const double kcd = r.kc * dt, kad = r.ka * dt;
   double* dst = r.to_u ? r.u : r.stage_out;
 #pragma unroll
@@ -195,9 +226,11 @@ __device__ __forceinline__ void rk_store_pre(const RKArgs& r, const Geo& G, int 
     double out = fma(r.a0, u0[v], fma(kad, acc[v], kcd * kv[v]));
     if (r.rd_us) out = fma(r.a1, r.stage_in[off], out);
     if (r.wr_acc) r.acc[off] = fma(r.b0, acc[v], r.b1 * kv[v]);
-    store_face_images(dst + v * G.npts, G, i, j, k, pm, out);
     outv[v] = out;
   }
+  int64_t dl[3];
+  const int nd = face_image_deltas(G, i, j, k, periodic_mask(G), dl);
+  store_point_images<NV>(dst, G.npts, q, nd, dl, outv);
 }
 
 RKArgs make_rk(const hd_plan* p, int scheme, int stage, double* u, const double* dt_dev);

@@ -367,9 +367,9 @@ __device__ __forceinline__ bool line_of(const SweepArgs& a, int& i, int& j, int&
 // along the locally periodic axes (the gradient stencils are axis-aligned).
 __device__ __forceinline__ void store_prim(double* prim, const Geo& G, int i, int j, int k,
                                            const double (&pv)[4]) {
-  const int mask = (G.periodic[0] ? 1 : 0) | (G.periodic[1] ? 2 : 0) | (G.periodic[2] ? 4 : 0);
-#pragma unroll
-  for (int f = 0; f < 4; ++f) store_face_images(prim + f * G.npts, G, i, j, k, mask, pv[f]);
+  int64_t dl[3];
+  const int nd = face_image_deltas(G, i, j, k, periodic_mask(G), dl);
+  store_point_images<4>(prim, G.npts, G.idx(i, j, k), nd, dl, pv);
 }
 
 template <int DIM, bool EXACT, int ROLE>
@@ -832,6 +832,9 @@ int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, co
   SweepArgs a = make_args(p, 2, u_stage, inc, 1, 0, tag, nseg);
   a.vflux = vflux;
   a.prim = prim;
+  // cost-attribution switches for profiling only (results are wrong with them set)
+  if (getenv_flag("HD_PROFILE_NO_DZ")) a.vflux = nullptr;
+  if (getenv_flag("HD_PROFILE_NO_PRIMS")) a.prim = nullptr;
   a.rk = make_rk(p, scheme, stage, u, dt_dev);
   if (p->mode == HD_MODE_EXACT) return HD_E_UNSUPPORTED;  // exact mode runs the unfused stage
   return launch_dim<2, false, ROLE_UPDATE>(p, a, nseg, s);
