@@ -297,10 +297,24 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, 2) gradflux_zm_kernel(
     const double vel[3] = {qz[0][2], qz[1][2], qz[2][2]};
     double val[VF_N];
     viscous_flux_point<EXACT>(gr, gT, vel, mu, q_coef, val);
+    // each field gets face images only along the axes it is differentiated along
     const int pm = periodic_mask(G);
+    const int g = G.g;
+    const int64_t q = G.idx(i, j, k);
+    const int64_t ax = (pm & 1) ? (i < g ? G.n[0] : (i >= G.n[0] - g ? -(int64_t)G.n[0] : 0)) : 0;
+    const int64_t ay = (pm & 2) ? (j < g ? (int64_t)G.n[1] * G.sy
+                                         : (j >= G.n[1] - g ? -(int64_t)G.n[1] * G.sy : 0)) : 0;
+    const int64_t az = (pm & 4) ? (k < g ? (int64_t)G.n[2] * sz
+                                         : (k >= G.n[2] - g ? -(int64_t)G.n[2] * sz : 0)) : 0;
 #pragma unroll
-    for (int f = 0; f < VF_N; ++f)
-      store_face_images(vf + (int64_t)f * np, G, i, j, k, pm & vf_axes(f), val[f]);
+    for (int f = 0; f < VF_N; ++f) {
+      double* F = vf + (int64_t)f * np + q;
+      F[0] = val[f];
+      const int axes = vf_axes(f);
+      if ((axes & 1) && ax) F[ax] = val[f];
+      if ((axes & 2) && ay) F[ay] = val[f];
+      if ((axes & 4) && az) F[az] = val[f];
+    }
   }
 }
 
