@@ -306,6 +306,11 @@ constexpr int SWEEP_THREADS = 64;
 #ifndef HD_SWEEP_FLUX_WINDOW
 #define HD_SWEEP_FLUX_WINDOW 0
 #endif
+// L1 prefetch of the divergence operands: measured slower (143.8 vs 140.3 ms/step
+// at 512^3) -- the prefetches compete for LSU issue and L1 with the loads that follow
+#ifndef HD_NO_DIV_PREFETCH
+#define HD_NO_DIV_PREFETCH 1
+#endif
 template <int DIM> struct SweepCfg {
   static constexpr bool smem_window = DIM != 0 && HD_SWEEP_SMEM_WINDOW_YZ;
   static constexpr int min_blocks = DIM == 0 ? HD_SWEEP_MIN_BLOCKS_X : HD_SWEEP_MIN_BLOCKS_YZ;
@@ -487,7 +492,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
     }
     const bool wr = c > c0;
     double* q = inc + (int64_t)(c - 1) * sd;
-    if constexpr (VROLE && !FWIN) {
+    if constexpr (VROLE && !FWIN && !HD_NO_DIV_PREFETCH) {
       if (wr && a.vflux)
         prefetch_divergence(a.vflux, G, base + (int64_t)(c - 1) * sd, ROLE == ROLE_VISC ? 3 : 4);
     }
