@@ -14,6 +14,15 @@ __device__ __forceinline__ double cd4(const double* __restrict__ s, int64_t st, 
   return (8.0 * (p1 - m1) + (m2 - p2)) * coef;
 }
 
+// ---- cp.async (LDGSTS): global -> shared without staging through registers ----
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // the same stencil on values already in registers / shared memory
 template <bool EXACT>
 __device__ __forceinline__ double cd4v(double m2, double m1, double p1, double p2, double coef) {

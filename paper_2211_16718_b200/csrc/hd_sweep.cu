@@ -311,6 +311,9 @@ constexpr int SWEEP_THREADS = 64;
 #ifndef HD_NO_DIV_PREFETCH
 #define HD_NO_DIV_PREFETCH 1
 #endif
+#ifndef HD_DIV_CPASYNC
+#define HD_DIV_CPASYNC 0
+#endif
 template <int DIM> struct SweepCfg {
   static constexpr bool smem_window = DIM != 0 && HD_SWEEP_SMEM_WINDOW_YZ;
   static constexpr int min_blocks = DIM == 0 ? HD_SWEEP_MIN_BLOCKS_X : HD_SWEEP_MIN_BLOCKS_YZ;
@@ -413,6 +416,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   __shared__ double ring[SMEM_WINDOW ? 5 * RV * SWEEP_THREADS : 1];
   double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
   auto slot = [&](int m) -> double* { return mine + ((m + 5) % 5) * (RV * SWEEP_THREADS); };
+  // cp.async staging of the viscous-divergence operands (HD_DIV_CPASYNC)
+  constexpr bool DSTAGE = VROLE && !FWIN && HD_DIV_CPASYNC && !EXACT;
+  constexpr int DMASK = ROLE == ROLE_VISC ? 3 : 4;
+  constexpr int DN = ROLE == ROLE_VISC ? 32 : 16;
+  __shared__ double dstage[DSTAGE ? DN * SWEEP_THREADS : 1];
+  double* const dsb = dstage + threadIdx.y * 32 + threadIdx.x;
   double wu[5][NV], wf[5][NV];
   // viscous flux window: position p -> slot(p) columns 9..12; F(c+1) enters at
   // iteration c from fpre (loaded one iteration earlier)
@@ -492,9 +501,32 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
     }
     const bool wr = c > c0;
     double* q = inc + (int64_t)(c - 1) * sd;
-    if constexpr (VROLE && !FWIN && !HD_NO_DIV_PREFETCH) {
+    if constexpr (VROLE && !FWIN && !HD_NO_DIV_PREFETCH && !DSTAGE) {
       if (wr && a.vflux)
         prefetch_divergence(a.vflux, G, base + (int64_t)(c - 1) * sd, ROLE == ROLE_VISC ? 3 : 4);
+    }
+    if constexpr (DSTAGE) {
+      // divergence operands of cell c-1 -> shared memory, consumed after the
+      // window's FP64 work (cp.async: no registers held meanwhile)
+      if (wr && a.vflux) {
+        const int64_t qc = base + (int64_t)(c - 1) * sd;
+        int o = 0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          if (!(DMASK & (1 << d))) continue;
+          const int64_t st = G.stride(d);
+#pragma unroll
+          for (int row = 1; row < NV; ++row) {
+            const double* f = a.vflux + (int64_t)vf_field(d, row) * np + qc;
+            cp_async8(dsb + (o + 0) * SWEEP_THREADS, f - 2 * st);
+            cp_async8(dsb + (o + 1) * SWEEP_THREADS, f - st);
+            cp_async8(dsb + (o + 2) * SWEEP_THREADS, f + st);
+            cp_async8(dsb + (o + 3) * SWEEP_THREADS, f + 2 * st);
+            o += 4;
+          }
+        }
+        cp_async_commit();
+      }
     }
     // ROLE_UPDATE: the RK inputs of cell c-1 (base state, accumulator) are
     // loaded here, a full window of FP64 work before the update consumes them
@@ -562,7 +594,22 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
             const int o = r * SWEEP_THREADS;
             val[r + 1] += (8.0 * (p1[o] - m1[o]) + (m2[o] - p2[o])) * coef;
           }
-        } else if (VROLE && a.vflux) {  // direct stencil loads (L1-prefetched above)
+        } else if (DSTAGE && a.vflux) {  // operands staged by cp.async at the top
+          cp_async_wait<0>();
+          int o = 0;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            if (!(DMASK & (1 << d))) continue;
+            const double coef = 1.0 / (12.0 * G.h[d]);
+#pragma unroll
+            for (int row = 1; row < NV; ++row) {
+              val[row] += cd4v<false>(dsb[o * SWEEP_THREADS], dsb[(o + 1) * SWEEP_THREADS],
+                                      dsb[(o + 2) * SWEEP_THREADS], dsb[(o + 3) * SWEEP_THREADS],
+                                      coef);
+              o += 4;
+            }
+          }
+        } else if (VROLE && a.vflux) {  // direct stencil loads
           add_viscous_divergence<EXACT>(a.vflux, G, base + (int64_t)(c - 1) * sd,
                                         ROLE == ROLE_VISC ? 3 : 4, val);
         }
@@ -616,14 +663,6 @@ static bool getenv_flag(const char* name) {
 }
 
 constexpr int XS_PAD = 5;  // row pitch of a staging tile (doubles): 40 B, conflict-free 64-bit reads
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <bool EXACT>
 __global__ void __launch_bounds__(SWEEP_THREADS, HD_SWEEP_MIN_BLOCKS_X) sweep_x_staged_kernel(
@@ -791,6 +830,10 @@ static SweepArgs make_args(const hd_plan* p, int dim, const double* u, double* i
   nseg = (int)((target + lines - 1) / lines);
   if (nseg < 1) nseg = 1;
   if (nseg > G.n[dim] / 8) nseg = G.n[dim] / 8 > 0 ? G.n[dim] / 8 : 1;
+  if (const char* e = getenv("HD_SWEEP_SEGMENTS")) {  // tests: results must not depend on it
+    const int want = atoi(e);
+    if (want >= 1 && want <= G.n[dim]) nseg = want;
+  }
   a.seg = (G.n[dim] + nseg - 1) / nseg;
   nseg = (G.n[dim] + a.seg - 1) / a.seg;
   return a;

@@ -111,6 +111,11 @@ def _as_device(fields) -> FieldSet:
     return FieldSet.from_numpy(fields)
 
 
+def _coerce(fields) -> FieldSet:
+    """A FieldSet of this package (reference FieldSets are wrapped, not moved)."""
+    return fields if isinstance(fields, FieldSet) else FieldSet.from_numpy(fields)
+
+
 def _reduce(fields: FieldSet, gas: GasModel, tag: int = 0) -> np.ndarray:
     plan = get_plan(fields.spec, gas)
     out = torch.empty(_lib.HD_RED_N, dtype=torch.float64, device=fields.data.device)
@@ -203,10 +208,14 @@ def _fusable(rhs, fields) -> bool:
 
 
 def rk3_tvd_step(fields: FieldSet, dt: float, rhs) -> FieldSet:
-    """One three-stage TVD Runge-Kutta step (timeint.py:168-178)."""
-    fields = _as_device(fields)
+    """One three-stage TVD Runge-Kutta step (timeint.py:168-178).
+
+    With a ``make_rhs`` closure the whole step is one fused device call; any
+    other rhs callable is composed stage by stage like the reference (torch
+    arithmetic on whatever device ``fields`` lives on)."""
+    fields = _coerce(fields)
     if _fusable(rhs, fields):
-        return _fused_step(fields, dt, rhs, "rk3")
+        return _fused_step(_as_device(fields), dt, rhs, "rk3")
     spec, layout = fields.spec, fields.layout
     r0 = _stage(rhs, fields, 0)
     u1 = FieldSet(spec, layout, fields.data + dt * r0.data)
@@ -217,10 +226,10 @@ def rk3_tvd_step(fields: FieldSet, dt: float, rhs) -> FieldSet:
 
 
 def rk4_step(fields: FieldSet, dt: float, rhs) -> FieldSet:
-    """One classical four-stage Runge-Kutta step (timeint.py:181-193)."""
-    fields = _as_device(fields)
+    """One classical four-stage Runge-Kutta step (timeint.py:181-193); see rk3_tvd_step."""
+    fields = _coerce(fields)
     if _fusable(rhs, fields):
-        return _fused_step(fields, dt, rhs, "rk4")
+        return _fused_step(_as_device(fields), dt, rhs, "rk4")
     spec, layout = fields.spec, fields.layout
     half = 0.5 * dt
     k1 = _stage(rhs, fields, 0)

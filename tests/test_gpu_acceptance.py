@@ -1,0 +1,109 @@
+"""The reference's acceptance criteria (pkg/tests/test_acceptance.py) run on the CUDA path.
+
+* fifth-order advected density wave, 32 -> 64 -> 128 (:119-146): order >= 4.5
+* fourth-order viscous operators on a shear profile, 32 -> 64 (:149-174): order >= 3.5
+* results independent of how lines are split into segments -- the analogue
+  of the reference's worker-count invariance (pkg/tests/test_upwind.py:107-111)
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+GAMMA = 1.4
+
+
+@pytest.fixture(scope="module")
+def hd():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2211_16718_b200 as hd
+
+    hd._lib.load(require_cuda=True)
+    return hd
+
+
+def _coords(n):
+    c = torch.arange(n, dtype=torch.float64, device="cuda") * (2 * math.pi / n)
+    return torch.meshgrid(c, c, c, indexing="ij")  # z, y, x
+
+
+def _from_prims(hd, spec, rho, u, v, w, p):
+    fs = hd.FieldSet.zeros(spec)
+    it = fs.interior()
+    it[0] = rho
+    it[1] = rho * u
+    it[2] = rho * v
+    it[3] = rho * w
+    it[4] = p / (GAMMA - 1.0) + 0.5 * rho * (u * u + v * v + w * w)
+    hd.fill_ghosts_periodic(fs)
+    return fs
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_fifth_order_advected_density(hd, mode):
+    wind, amp, p0 = 0.7, 0.3, 1.0
+    errs = []
+    for n in (32, 64, 128):
+        spec = hd.GridSpec((n, n, n))
+        z, y, x = _coords(n)
+        rho = 1.0 + amp * torch.sin(x)
+        one = torch.ones_like(rho)
+        fs = _from_prims(hd, spec, rho, wind * one, 0 * one, 0 * one, p0 * one)
+        inc = hd.hyperbolic_rhs(fs, hd.GasModel(), mode=mode).interior()
+        drho = amp * torch.cos(x)
+        want = torch.zeros_like(inc)
+        want[0] = -wind * drho
+        want[1] = -wind * wind * drho
+        want[4] = -0.5 * wind ** 3 * drho
+        errs.append((inc - want).abs().max().item())
+    o1, o2 = math.log2(errs[0] / errs[1]), math.log2(errs[1] / errs[2])
+    assert o1 >= 4.5 and o2 >= 4.5, (o1, o2)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_fourth_order_viscous_on_shear(hd, mode):
+    mu = 0.01
+    errs_d, errs_m, errs_e = [], [], []
+    for n in (32, 64):
+        spec = hd.GridSpec((n, n, n))
+        z, y, x = _coords(n)
+        g = spec.ghost_width
+        buf = torch.zeros(spec.shape, dtype=torch.float64, device="cuda")
+        buf[g:-g, g:-g, g:-g] = torch.sin(y)
+        hd.fill_ghosts_array(buf, spec.n, g)
+        got = hd.central_derivative_4(buf, 1, spec.spacing[1])
+        errs_d.append((got - torch.cos(y)).abs().max().item())
+        zero = torch.zeros_like(y)
+        fs = _from_prims(hd, spec, torch.ones_like(y), torch.sin(y), zero, zero,
+                         torch.full_like(y, 1.0 / GAMMA))
+        inc = hd.parabolic_rhs(fs, hd.GasModel(mu=mu), mode=mode).interior()
+        errs_m.append((inc[1] + mu * torch.sin(y)).abs().max().item())
+        errs_e.append((inc[4] - mu * torch.cos(2.0 * y)).abs().max().item())
+    for e in (errs_d, errs_m, errs_e):
+        assert math.log2(e[0] / e[1]) >= 3.5
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_segment_split_invariance(hd, monkeypatch, mode):
+    """One thread per line, or the line cut into 4 or 7 segments: every
+    interface is evaluated from the same window, so the step is bitwise equal."""
+    spec = hd.GridSpec((32, 64, 56))
+    rng = np.random.default_rng(5)
+    shape = spec.interior_shape
+    rho = torch.from_numpy(0.8 + 0.4 * rng.random(shape)).cuda()
+    vel = [torch.from_numpy(0.3 * rng.standard_normal(shape)).cuda() for _ in range(3)]
+    p = torch.from_numpy(0.8 + 0.4 * rng.random(shape)).cuda()
+    fs = _from_prims(hd, spec, rho, *vel, p)
+    outs = []
+    for segs in ("1", "4", "7"):
+        monkeypatch.setenv("HD_SWEEP_SEGMENTS", segs)
+        hd.release_plans()
+        res = hd.advance(fs, hd.GasModel(mu=0.01), hd.TimeParams(scheme="rk4", cfl=0.3, max_steps=2),
+                         mode=mode)
+        outs.append(res.fields.interior().cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
