@@ -662,14 +662,33 @@ static bool getenv_flag(const char* name) {
   return v && v[0] && v[0] != '0';
 }
 
-constexpr int XS_PAD = 5;  // row pitch of a staging tile (doubles): 40 B, conflict-free 64-bit reads
+// Chunk of XC positions per row; staging tiles have row pitch XC + 1 doubles
+// (odd: conflict-free 64-bit access).  XC <= 2 would leave room for a
+// shared-memory window ring (as in the y/z sweeps) but measured slower at
+// 512^3 (149-165 vs 141 ms/step): XC = 4 with a register window.
+#ifndef HD_XCHUNK
+#define HD_XCHUNK 4
+#endif
+constexpr int XC = HD_XCHUNK;
+#ifndef HD_XPAD
+#define HD_XPAD (HD_XCHUNK + 1)
+#endif
+#ifndef HD_XOUT_STAGE
+#define HD_XOUT_STAGE 1
+#endif
+constexpr int XS_PAD = HD_XPAD;
+constexpr bool XOUT_STAGE = HD_XOUT_STAGE;
+constexpr bool XRING = XC <= 2;
+constexpr int XMINB = XRING ? HD_SWEEP_MIN_BLOCKS_YZ : HD_SWEEP_MIN_BLOCKS_X;
 
 template <bool EXACT>
-__global__ void __launch_bounds__(SWEEP_THREADS, HD_SWEEP_MIN_BLOCKS_X) sweep_x_staged_kernel(
-    const SweepArgs a) {
+__global__ void __launch_bounds__(SWEEP_THREADS, XMINB) sweep_x_staged_kernel(const SweepArgs a) {
   constexpr int WARPS = SWEEP_THREADS / 32;
   __shared__ double xin[WARPS][2][NV][32 * XS_PAD];
-  __shared__ double xout[WARPS][NV][32 * XS_PAD];
+  __shared__ double xout[XOUT_STAGE ? WARPS : 1][NV][32 * XS_PAD];
+  __shared__ double ring[XRING ? 5 * 9 * SWEEP_THREADS : 1];
+  double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
+  auto slot = [&](int m) -> double* { return mine + ((m + 5) % 5) * (9 * SWEEP_THREADS); };
   const Geo& G = a.geo;
   const int lane = threadIdx.x, w = threadIdx.y;
   const int j0 = blockIdx.x * 32;  // launch guarantees n_y % 32 == 0
@@ -687,15 +706,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS, HD_SWEEP_MIN_BLOCKS_X) sweep_x_
   const int power = a.ph.power;
   const int p0 = c0 - 3;  // first position entering the window
 
-  // chunk t holds positions p0 + 4t .. p0 + 4t + 3 of all 32 rows
+  // chunk t holds positions p0 + XC t .. p0 + XC t + XC-1 of all 32 rows; lane l
+  // copies row (32/XC) i + l/XC, position l % XC (consecutive lanes: consecutive x)
+  constexpr int RPI = 32 / XC;  // rows per copy instruction
   auto issue = [&](int t) {
     const int buf = t & 1;
-    const int xo = lane & 3;
-    const int p = p0 + 4 * t + xo;
+    const int xo = lane % XC;
+    const int p = p0 + XC * t + xo;
     if (p <= c1 + 2) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = 8 * i + (lane >> 2);
+      for (int i = 0; i < XC; ++i) {
+        const int r = RPI * i + lane / XC;
         const double* src = a.u + row0 + (int64_t)r * sy + p;
 #pragma unroll
         for (int v = 0; v < NV; ++v) cp_async8(&xin[w][buf][v][r * XS_PAD + xo], src + v * np);
@@ -705,25 +726,32 @@ __global__ void __launch_bounds__(SWEEP_THREADS, HD_SWEEP_MIN_BLOCKS_X) sweep_x_
   };
   auto take = [&](int p, double (&uu)[NV], double (&ff)[NV]) {
     const int q = p - p0;
-    const double* s = &xin[w][(q >> 2) & 1][0][lane * XS_PAD + (q & 3)];
+    const double* s = &xin[w][(q / XC) & 1][0][lane * XS_PAD + (q % XC)];
 #pragma unroll
     for (int v = 0; v < NV; ++v) uu[v] = s[v * 32 * XS_PAD];
     double inv, pv[4];
     point_flux<0, EXACT>(uu, gm1, ff, inv, pv);
+    if constexpr (XRING) {
+      double* sp = slot(p);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sp[v * SWEEP_THREADS] = uu[v];
+#pragma unroll
+      for (int v = 1; v < NV; ++v) sp[(NV - 1 + v) * SWEEP_THREADS] = ff[v];
+    }
     if (a.check && p >= 0 && p < nd) {
       if (!(uu[0] > 0.0)) latch_error(a.err, a.tag, 1, base + p);
       else if (!(pv[3] > 0.0)) latch_error(a.err, a.tag, 2, base + p);
     }
   };
-  // out chunk: cells c0 + 4 t .. +3; d[v] staged, flushed coalesced as inc = old - d
+  // out chunk: cells c0 + XC t .. ; d[v] staged, flushed coalesced as inc = old - d
   auto flush = [&](int t) {
     __syncwarp();
-    const int xo = lane & 3;
-    const int m = c0 + 4 * t + xo;
+    const int xo = lane % XC;
+    const int m = c0 + XC * t + xo;
     if (m < c1) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = 8 * i + (lane >> 2);
+      for (int i = 0; i < XC; ++i) {
+        const int r = RPI * i + lane / XC;
         double* dst = a.inc + row0 + (int64_t)r * sy + m;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
@@ -738,36 +766,61 @@ __global__ void __launch_bounds__(SWEEP_THREADS, HD_SWEEP_MIN_BLOCKS_X) sweep_x_
   };
 
   double wu[5][NV], wf[5][NV];
+  // Entering chunk t (its first position is consumed): wait for it -- it was
+  // issued when chunk t-1 was entered -- then issue chunk t+1 into the buffer
+  // chunk t-1 has vacated.  Positions p0 .. p0+3 fill the window first.
   issue(0);
-  issue(1);
-  cp_async_wait<1>();
-  __syncwarp();
 #pragma unroll
-  for (int q = 0; q < 4; ++q) take(p0 + q, wu[q + 1], wf[q + 1]);
+  for (int q = 0; q < 4; ++q) {
+    if (q % XC == 0) {
+      cp_async_wait<0>();
+      __syncwarp();
+      issue(q / XC + 1);
+    }
+    take(p0 + q, wu[q + 1], wf[q + 1]);
+  }
 
   double lu[NV], lf[NV], fprev[NV];
   for (int c = c0 - 1; c <= c1; ++c) {
     const int p = c + 2;
-    if (((p - p0) & 3) == 0) {  // entering chunk t: it has landed; start t+1
+    if ((p - p0) % XC == 0) {
       cp_async_wait<0>();
       __syncwarp();
-      issue(((p - p0) >> 2) + 1);
+      issue((p - p0) / XC + 1);
     }
+    if constexpr (!XRING) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        wu[q][v] = wu[q + 1][v];
-        wf[q][v] = wf[q + 1][v];
-      }
+        for (int v = 0; v < NV; ++v) {
+          wu[q][v] = wu[q + 1][v];
+          wf[q][v] = wf[q + 1][v];
+        }
+    }
     take(p, wu[4], wf[4]);
     double ru[NV], rf[NV], nu[NV], nf[NV];
+    if constexpr (XRING) {
+      const double* w0 = slot(c - 2);
+      const double* w1 = slot(c - 1);
+      const double* w2 = slot(c);
+      const double* w3 = slot(c + 1);
+      const double* w4 = slot(c + 2);
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
-      recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
+      for (int v = 0; v < 2 * NV - 1; ++v) {
+        double l, r;
+        recon_pair<EXACT>(w0[v * SWEEP_THREADS], w1[v * SWEEP_THREADS], w2[v * SWEEP_THREADS],
+                          w3[v * SWEEP_THREADS], w4[v * SWEEP_THREADS], eps, power, l, r);
+        if (v < NV) { nu[v] = l; ru[v] = r; }
+        else { nf[v - NV + 1] = l; rf[v - NV + 1] = r; }
+      }
+    } else {
 #pragma unroll
-    for (int v = 1; v < NV; ++v)
-      recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
+      for (int v = 0; v < NV; ++v)
+        recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
+#pragma unroll
+      for (int v = 1; v < NV; ++v)
+        recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
+    }
     nf[0] = nu[1];
     rf[0] = ru[1];
     if (c >= c0) {
@@ -775,15 +828,22 @@ __global__ void __launch_bounds__(SWEEP_THREADS, HD_SWEEP_MIN_BLOCKS_X) sweep_x_
       roe_flux<0, EXACT>(lu, ru, lf, rf, a.ph, flux);
       if (c > c0) {
         const int m = c - 1;
-        const int oo = (m - c0) & 3;
+        const int oo = (m - c0) % XC;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           double d;
           if constexpr (EXACT) d = xm(xs(flux[v], fprev[v]), a.inv_dx);
           else d = (flux[v] - fprev[v]) * a.inv_dx;
-          xout[w][v][lane * XS_PAD + oo] = d;
+          if constexpr (XOUT_STAGE) {
+            xout[w][v][lane * XS_PAD + oo] = d;
+          } else {
+            double* dst = a.inc + base + m + v * np;
+            const double old = a.accumulate ? *dst : 0.0;
+            if constexpr (EXACT) *dst = xs(old, d);
+            else *dst = old - d;
+          }
         }
-        if (oo == 3 || m == c1 - 1) flush((m - c0) >> 2);
+        if (XOUT_STAGE && (oo == XC - 1 || m == c1 - 1)) flush((m - c0) / XC);
       }
 #pragma unroll
       for (int v = 0; v < NV; ++v) fprev[v] = flux[v];
