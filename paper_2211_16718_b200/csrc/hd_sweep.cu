@@ -411,7 +411,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   // larger ring leaves too little L1 for the other streams of the kernel;
   // the default reads the stencil directly, operands prefetched into L1.)
   constexpr bool VROLE = ROLE != ROLE_PLAIN;
-  constexpr bool FWIN = VROLE && HD_SWEEP_FLUX_WINDOW;
+  constexpr bool FWIN = VROLE && (HD_SWEEP_FLUX_WINDOW == 3 ||
+                                  (HD_SWEEP_FLUX_WINDOW == 1 && ROLE == ROLE_VISC) ||
+                                  (HD_SWEEP_FLUX_WINDOW == 2 && ROLE == ROLE_UPDATE));
   constexpr int RV = FWIN ? 13 : 9;  // values per ring slot
   __shared__ double ring[SMEM_WINDOW ? 5 * RV * SWEEP_THREADS : 1];
   double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
