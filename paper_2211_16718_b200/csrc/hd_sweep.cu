@@ -78,12 +78,14 @@ __device__ __forceinline__ void recon_pair(double q0, double q1, double q2, doub
     //   6 (c_k - q2) = 5D1-2D0, D1+2D2, 4D2-D3 (left) and 2D3-5D2, -(D2+2D1),
     //   D0-4D1 (right).
     const double D0 = q1 - q0, D1 = q2 - q1, D2 = q3 - q2, D3 = q4 - q3;
-    const double t1 = D1 - D0, t2 = D2 - D1, t3 = D3 - D2;
-    const double s1 = fma(3.0, D1, -D0), s2 = D1 + D2, s3 = fma(-3.0, D2, D3);
-    const double eps12 = 12.0 * eps;
-    const double d1 = fma(13.0 * t1, t1, fma(3.0 * s1, s1, eps12));
-    const double d2 = fma(13.0 * t2, t2, fma(3.0 * s2, s2, eps12));
-    const double d3 = fma(13.0 * t3, t3, fma(3.0 * s3, s3, eps12));
+    // expanded: 12 beta1 = 13 t1^2 + 3 s1^2 = 4 (10 D1^2 - 11 D0 D1 + 4 D0^2), and
+    // likewise 3 beta2 = 4 D1^2 - 5 D1 D2 + 4 D2^2, 3 beta3 = 10 D2^2 - 11 D2 D3 + 4 D3^2
+    // (weights scaled by a common factor 3, eps with them)
+    const double S0 = D0 * D0, S1 = D1 * D1, S2 = D2 * D2, S3 = D3 * D3;
+    const double eps3 = 3.0 * eps;
+    const double d1 = fma(10.0, S1, fma(-11.0 * D0, D1, fma(4.0, S0, eps3)));
+    const double d2 = fma(4.0, S1 + S2, fma(-5.0 * D1, D2, eps3));
+    const double d3 = fma(10.0, S2, fma(-11.0 * D2, D3, fma(4.0, S3, eps3)));
     double e1 = d1, e2 = d2, e3 = d3;
     for (int q = 0; q < power - 1; ++q) {
       e1 *= d1;
