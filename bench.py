@@ -32,6 +32,19 @@ ALG_BYTES_PER_PT_STEP = 680.0      # compulsory SoA traffic of a
 ALG_FLOPS_PER_PT_STEP = 17.9e3 + 1550.0  # flops + div/sqrt counted as one
 SWEEP_FLOPS_PER_PT = 1406.0 + 125.0 + 3.0 + 10.0  # per interface (K:97-204) + flux components
 MU = 0.006
+# Algorithmic (bytes, reference flops) per interior point and launch of each stage kernel
+# (fast mode): the reference counts 1,406 flops + 125 div + 3 sqrt per interface
+# + ~10 for the flux components; central differences 6 flops each.
+_SW = SWEEP_FLOPS_PER_PT
+KERNEL_COST = {
+    "sweep_x": (80.0, _SW),                       # u 40 + inc 40 (overwrite)
+    "sweep_y": (176.0, _SW + 8 * 7),              # u 40 + inc RMW 80 + F_x, F_y (7 fields) 56
+    "sweep_z": (304.0, _SW + 4 * 7 + 15 + 12),    # u, inc, u_n, acc 160 + F_z 32 | out, acc 80 + prims 32
+    "gradflux": (104.0, 12 * 6 + 40),             # prims 32 | 9 flux fields 72
+    "prims": (72.0, 15.0),
+    "divergence": (192.0, 12 * 7 + 15),           # exact mode: 9 fields + inc, u, acc | out, acc
+    "reduce": (40.0, 30.0),
+}
 
 
 def parse():
@@ -168,32 +181,6 @@ def fp64_peak(hd, torch):
     return 2.0 * 8 * iters * threads * blocks / sec / 1e12
 
 
-def time_kernels(hd, torch, plan, u, reps=3):
-    """CUDA-event durations of the individual kernels on the launching stream."""
-    inc = plan.fields(hd._lib.HD_BUF_INC, 5)
-    res = {}
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for dim, name in enumerate(("sweep_x", "sweep_y", "sweep_z")):
-        acc = dim != 0  # as in the stage pipeline: the x sweep overwrites inc, y/z accumulate
-        plan.hyper_sweep(dim, u, inc, acc)
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(reps):
-            plan.hyper_sweep(dim, u, inc, acc)
-        e1.record()
-        torch.cuda.synchronize()
-        res[name] = e0.elapsed_time(e1) / reps
-    plan.parabolic_rhs(u, inc)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        plan.parabolic_rhs(u, inc)
-    e1.record()
-    torch.cuda.synchronize()
-    res["viscous"] = e0.elapsed_time(e1) / reps
-    return res
-
-
 def main():
     args = parse()
     if args.impl == "reference":
@@ -246,6 +233,9 @@ def main():
 
     # ---- timed region -------------------------------------------------------------
     L = hd._lib.load()
+    plan = hd.get_plan(lspec, gas, periodic=(True, True, world == 1))
+    plan.timer_read()  # drop warm-up records
+    plan.timer_enable(True)  # CUDA events around every stage kernel, on its stream
     launches0 = L.hd_launch_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -255,6 +245,8 @@ def main():
         e1.record()
         barrier()
     launches = L.hd_launch_counter() - launches0
+    ktimes = plan.timer_read()
+    plan.timer_enable(False)
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -265,19 +257,23 @@ def main():
     recs = res.records
     state = res.fields
 
-    # ---- kernel timing for the roofline (same stream, after the timed region) ---
-    plan = hd.get_plan(lspec, gas, periodic=(True, True, world == 1))
-    kern = time_kernels(hd, torch, plan, state.data)
+    # ---- roofline of the dominant kernel, timed inside the timed region ---------------
     peak_fp64 = fp64_peak(hd, torch)
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
         peaks = json.load(fh)
     hbm_peak = float(peaks["hbm_gbs"])
-    top = max(("sweep_x", "sweep_y", "sweep_z"), key=lambda k: kern[k])
     lpts = lspec.interior_points
-    # read u (40 B) + inc write (x: 40 B) or read-modify-write (y, z: 80 B) per point
-    sweep_bytes = lpts * (80.0 if top == "sweep_x" else 120.0)
-    sweep_flops = lpts * SWEEP_FLOPS_PER_PT
-    achieved_gbs = sweep_bytes / (kern[top] / 1e3) / 1e9
+    kernels = {}
+    for kind, (tot, cnt) in ktimes.items():
+        if not cnt:
+            continue
+        avg = tot / cnt
+        b, f = KERNEL_COST.get(kind, (0.0, 0.0))
+        kernels[kind] = {"avg_ms": avg, "launches": cnt, "share": tot / ms,
+                         "GB_s": lpts * b / (avg / 1e3) / 1e9,
+                         "TFLOP_s": lpts * f / (avg / 1e3) / 1e12}
+    top = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches"])
+    kt = kernels[top]
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "sweep_dram_bytes.json")
     if os.path.exists(tfile):
@@ -286,15 +282,15 @@ def main():
         if tr.get("n") == n and world == 1 and tr.get("kernel") == top:
             traffic = tr.get("bytes_per_launch")
     roofline = {
-        "bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-        "frac": achieved_gbs / hbm_peak, "traffic": traffic, "kernel": top,
-        "note": "FP64-pipe-bound stencil: see fp64 (frac of measured DFMA peak)",
-        "fp64": {"achieved_tflops": sweep_flops / (kern[top] / 1e3) / 1e12,
-                 "peak_tflops_measured": peak_fp64,
-                 "frac": sweep_flops / (kern[top] / 1e3) / 1e12 / peak_fp64},
+        "bound": "hbm", "achieved": kt["GB_s"], "peak": hbm_peak, "unit": "GB/s",
+        "frac": kt["GB_s"] / hbm_peak, "traffic": traffic, "kernel": top,
+        "note": ("the stencil is FP64-pipe-bound: fp64.frac is the binding one; algorithmic "
+                 "bytes/flops per point in KERNEL_COST (bench.py) and DESIGN.md sec. 3"),
+        "fp64": {"achieved_tflops": kt["TFLOP_s"], "peak_tflops_measured": peak_fp64,
+                 "frac": kt["TFLOP_s"] / peak_fp64},
         "step": {"hbm_frac": value / world * ALG_BYTES_PER_PT_STEP / (hbm_peak * 1e9),
                  "fp64_frac": value / world * ALG_FLOPS_PER_PT_STEP / (peak_fp64 * 1e12)},
-        "kernel_ms": kern,
+        "kernels": kernels,
     }
 
     # ---- end-to-end through the public API with host buffers ------------------------

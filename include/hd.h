@@ -188,6 +188,21 @@ int hd_commit_time(hd_plan* plan, double* ctx, void* stream);
 int hd_error_read(hd_plan* plan, uint64_t* key, void* stream);
 int hd_error_clear(hd_plan* plan, void* stream);
 
+/* ---- per-kernel timing ------------------------------------------------------- */
+/* With the timer on, every launch of the stage pipeline and of hd_reduce_state is
+ * bracketed by CUDA events on its stream; hd_timer_read synchronises, returns the
+ * summed milliseconds and launch counts per kind (HD_TK_*) and resets. */
+#define HD_TK_SWEEP_X 0
+#define HD_TK_SWEEP_Y 1
+#define HD_TK_SWEEP_Z 2
+#define HD_TK_GRADFLUX 3
+#define HD_TK_PRIMS 4
+#define HD_TK_DIVERGENCE 5
+#define HD_TK_REDUCE 6
+#define HD_TK_N 7
+int hd_timer_enable(hd_plan* plan, int on);
+int hd_timer_read(hd_plan* plan, double* ms, int64_t* count, int nkinds);
+
 /* Kernels launched by this library since load (monotonic; for launch accounting). */
 int64_t hd_launch_counter(void);
 

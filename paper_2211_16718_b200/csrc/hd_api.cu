@@ -15,6 +15,8 @@
 #include <atomic>
 #include <cstring>
 #include <new>
+#include <utility>
+#include <vector>
 
 #include "hd_internal.cuh"
 
@@ -83,6 +85,8 @@ int sweeps(hd_plan* p, int dmask, const double* us, double* inc, bool first_over
 }
 
 int nstages(int scheme) { return scheme == HD_SCHEME_RK3 ? 3 : 4; }
+
+void timer_free(void* t);  // defined with the Timer below
 
 // stage s > 0 reads the ping-pong half (s-1)%2 of the STAGE buffer (see make_rk)
 const double* stage_input(hd_plan* p, int stage, const double* u) {
@@ -172,6 +176,7 @@ int hd_plan_create(const hd_geom* geom, const hd_gas* gas, const hd_weno* weno, 
 }
 
 int hd_plan_destroy(hd_plan* p) {
+  if (p) timer_free(p->timer);
   delete p;
   return HD_OK;
 }
@@ -220,6 +225,81 @@ int hd_rhs(hd_plan* p, double* u, double* inc, void* stream) {
   return rc;
 }
 
+}  // extern "C"
+
+// ---- per-kernel event timer (hd_timer_*): event pairs around each launch of the
+// stage pipeline, summed per kernel kind on read.  Off by default (zero cost).
+namespace {
+struct Timer {
+  bool on = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> used;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t take() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  ~Timer() {
+    for (auto& u : used) {
+      cudaEventDestroy(u.second.first);
+      cudaEventDestroy(u.second.second);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+Timer* timer_of(hd_plan* p) { return (Timer*)p->timer; }
+void timer_free(void* t) { delete (Timer*)t; }
+
+// run launch expression `fn` bracketed by events when the timer is on
+template <class F>
+int timed(hd_plan* p, int kind, cudaStream_t s, F fn) {
+  Timer* t = timer_of(p);
+  if (!t || !t->on) return fn();
+  cudaEvent_t a = t->take(), b = t->take();
+  cudaEventRecord(a, s);
+  const int rc = fn();
+  cudaEventRecord(b, s);
+  t->used.push_back({kind, {a, b}});
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int hd_timer_enable(hd_plan* p, int on) {
+  if (!p) return HD_E_ARG;
+  if (!p->timer) p->timer = new (std::nothrow) Timer;
+  if (!p->timer) return HD_E_ARG;
+  timer_of(p)->on = on != 0;
+  return HD_OK;
+}
+
+int hd_timer_read(hd_plan* p, double* ms, int64_t* count, int nkinds) {
+  if (!p || !ms || !count || nkinds < HD_TK_N) return HD_E_ARG;
+  for (int k = 0; k < nkinds; ++k) {
+    ms[k] = 0.0;
+    count[k] = 0;
+  }
+  Timer* t = timer_of(p);
+  if (!t) return HD_OK;
+  for (auto& u : t->used) {
+    if (cudaEventSynchronize(u.second.second) != cudaSuccess) return HD_E_CUDA;
+    float f = 0.0f;
+    cudaEventElapsedTime(&f, u.second.first, u.second.second);
+    ms[u.first] += f;
+    count[u.first] += 1;
+    t->pool.push_back(u.second.first);
+    t->pool.push_back(u.second.second);
+  }
+  t->used.clear();
+  return HD_OK;
+}
+
 int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const double* dt_dev,
                   int64_t tag, void* stream) {
   if (!p || !u || (scheme != HD_SCHEME_RK3 && scheme != HD_SCHEME_RK4)) return HD_E_ARG;
@@ -239,35 +319,46 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   const bool zx = !p->geo.periodic[2];  // z ghosts come from a halo exchange
   // LOCAL: sweeps that read no z ghosts (a z-halo exchange of `us` can be in flight)
   if (parts & HD_PART_LOCAL) {
-    rc = launch_sweep(p, 0, us, inc, 0, 1, t, s);
-    if (!rc && exact) rc = launch_sweep(p, 1, us, inc, 1, 0, t, s);
+    rc = timed(p, HD_TK_SWEEP_X, s, [&] { return launch_sweep(p, 0, us, inc, 0, 1, t, s); });
+    if (!rc && exact)
+      rc = timed(p, HD_TK_SWEEP_Y, s, [&] { return launch_sweep(p, 1, us, inc, 1, 0, t, s); });
   }
   // PRIMS (fast): viscous primitives of the stage input over the whole box;
   // otherwise they come from the previous stage's update kernel
-  if (!rc && (parts & HD_PART_PRIMS) && !exact && visc) rc = launch_prims(p, us, s);
+  if (!rc && (parts & HD_PART_PRIMS) && !exact && visc)
+    rc = timed(p, HD_TK_PRIMS, s, [&] { return launch_prims(p, us, s); });
   // HALO (reads the z ghosts of `us`)
   //   exact: z sweep, primitives of the whole box, viscous fluxes
   //   fast:  primitives of exchanged ghost planes, viscous fluxes
   if (!rc && (parts & HD_PART_HALO)) {
     if (exact) {
-      rc = launch_sweep(p, 2, us, inc, 1, 0, t, s);
-      if (!rc && visc) rc = launch_prims(p, us, s);
+      rc = timed(p, HD_TK_SWEEP_Z, s, [&] { return launch_sweep(p, 2, us, inc, 1, 0, t, s); });
+      if (!rc && visc) rc = timed(p, HD_TK_PRIMS, s, [&] { return launch_prims(p, us, s); });
     } else if (visc && zx) {
       const int g = p->geo.g, nz = p->geo.n[2];
-      rc = launch_prims_planes(p, us, 0, g, s);
-      if (!rc) rc = launch_prims_planes(p, us, nz + g, nz + 2 * g, s);
+      rc = timed(p, HD_TK_PRIMS, s, [&] {
+        int r = launch_prims_planes(p, us, 0, g, s);
+        return r ? r : launch_prims_planes(p, us, nz + g, nz + 2 * g, s);
+      });
     }
-    if (!rc && visc) rc = launch_gradflux(p, s);
+    if (!rc && visc) rc = timed(p, HD_TK_GRADFLUX, s, [&] { return launch_gradflux(p, s); });
   }
   // MID (fast): y sweep + D_x F_x + D_y F_y (no z ghosts of the fluxes read)
-  if (!rc && (parts & HD_PART_MID) && !exact) rc = launch_sweep_visc(p, us, inc, vflux, t, s);
+  if (!rc && (parts & HD_PART_MID) && !exact)
+    rc = timed(p, HD_TK_SWEEP_Y, s, [&] { return launch_sweep_visc(p, us, inc, vflux, t, s); });
   // UPDATE (reads the z ghosts of the viscous z-flux group)
   //   exact: divergence in the viscous.py:112-120 order + RK update
   //   fast:  z sweep + D_z F_z + RK update + primitives of the new state
   if (!rc && (parts & HD_PART_UPDATE)) {
     if (!dt_dev) return HD_E_ARG;
-    rc = exact ? launch_divergence(p, visc ? 7 : 0, inc, nullptr, 1, scheme, stage, u, dt_dev, s)
-               : launch_sweep_update(p, us, inc, vflux, prim, scheme, stage, u, dt_dev, t, s);
+    if (exact)
+      rc = timed(p, HD_TK_DIVERGENCE, s, [&] {
+        return launch_divergence(p, visc ? 7 : 0, inc, nullptr, 1, scheme, stage, u, dt_dev, s);
+      });
+    else
+      rc = timed(p, HD_TK_SWEEP_Z, s, [&] {
+        return launch_sweep_update(p, us, inc, vflux, prim, scheme, stage, u, dt_dev, t, s);
+      });
   }
   return rc;
 }
@@ -292,7 +383,7 @@ int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag
 int hd_reduce_state(hd_plan* p, const double* u, double* out, int64_t tag, void* stream) {
   if (!p || !u || !out) return HD_E_ARG;
   if (!p->ws) return HD_E_WORKSPACE;
-  return launch_reduce(p, u, out, tag, S(stream));
+  return timed(p, HD_TK_REDUCE, S(stream), [&] { return launch_reduce(p, u, out, tag, S(stream)); });
 }
 
 int hd_error_read(hd_plan* p, uint64_t* key, void* stream) {

@@ -103,6 +103,7 @@ struct hd_plan {
   int64_t off[HD_NBUF];
   int device;
   int sm_count;
+  void* timer;  // per-kernel event timer (hd_timer_enable), owned
 };
 
 namespace hd {

@@ -162,6 +162,17 @@ class Plan:
     def commit_time(self, ctx) -> None:
         _lib.check(self.L.hd_commit_time(self.h, _ptr(ctx), _stream_ptr()), "hd_commit_time")
 
+    def timer_enable(self, on: bool = True) -> None:
+        _lib.check(self.L.hd_timer_enable(self.h, int(on)), "hd_timer_enable")
+
+    def timer_read(self) -> dict:
+        """{kind: (total ms, launches)} since the last read (CUDA events around each launch)."""
+        n = len(_lib.TIMER_KINDS)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        _lib.check(self.L.hd_timer_read(self.h, ms, cnt, n), "hd_timer_read")
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(_lib.TIMER_KINDS)}
+
     def error_key(self) -> int:
         key = ctypes.c_uint64(0)
         _lib.check(self.L.hd_error_read(self.h, ctypes.byref(key), _stream_ptr()), "hd_error_read")
