@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-n", type=int, default=128)
+    ap.add_argument("--dims", default=None,
+                    help="block decomposition px,py,pz for N>1 (default: z slabs 1,1,N)")
     return ap.parse_args()
 
 
@@ -205,7 +207,7 @@ def main():
     # ---- initial condition (identical on every rank; each keeps its z slab) --
     ic = hd.make_initial_condition(spec, hd.HitParams(), backend="torch")
     if world > 1:
-        dims = (1, 1, world)
+        dims = tuple(int(x) for x in args.dims.split(",")) if args.dims else (1, 1, world)
         lay = hd.decompose(spec, dims)[rank]
         state = hd.scatter(ic, [lay])[0]
         halo = hd.DistHalo(lay)
@@ -233,7 +235,7 @@ def main():
 
     # ---- timed region -------------------------------------------------------------
     L = hd._lib.load()
-    plan = hd.get_plan(lspec, gas, periodic=(True, True, world == 1))
+    plan = hd.get_plan(lspec, gas, periodic=halo.periodic if halo else (True, True, True))
     plan.timer_read()  # drop warm-up records
     plan.timer_enable(True)  # CUDA events around every stage kernel, on its stream
     launches0 = L.hd_launch_counter()
@@ -333,7 +335,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"HIT decay {n}^3, WENO5+Roe, 4th-order viscous, RK4, CFL 0.4",
                        "grid": n, "scheme": "rk4", "cfl": 0.4, "mu": MU, "mode": args.mode,
-                       "parallelism": f"z-slabs x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"blocks {'x'.join(map(str, lay.dims))}" if world > 1
+                                       else "single GPU"),
                        "l2": "state 5.6 GB >> 126 MB L2 (no flush needed)",
                        "ic": "HIT (HitParams defaults) synthesised on the GPU (torch backend)"},
             "gpu_launches": int(launches),

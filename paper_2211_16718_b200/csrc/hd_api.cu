@@ -305,8 +305,6 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   if (!p || !u || (scheme != HD_SCHEME_RK3 && scheme != HD_SCHEME_RK4)) return HD_E_ARG;
   if (!p->ws) return HD_E_WORKSPACE;
   if (stage < 0 || stage >= nstages(scheme)) return HD_E_ARG;
-  // the fused pipeline decomposes along z only (x and y wrap locally)
-  if (!p->geo.periodic[0] || !p->geo.periodic[1]) return HD_E_UNSUPPORTED;
   cudaStream_t s = S(stream);
   const double* us = stage_input(p, stage, u);
   double* inc = buf(p, HD_BUF_INC);
@@ -317,6 +315,7 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   double* prim = visc ? buf(p, HD_BUF_PRIM) : nullptr;
   double* vflux = visc ? buf(p, HD_BUF_VFLUX) : nullptr;
   const bool zx = !p->geo.periodic[2];  // z ghosts come from a halo exchange
+  const bool xyx = !p->geo.periodic[0] || !p->geo.periodic[1];  // so do x and/or y ghosts
   // LOCAL: sweeps that read no z ghosts (a z-halo exchange of `us` can be in flight)
   if (parts & HD_PART_LOCAL) {
     rc = timed(p, HD_TK_SWEEP_X, s, [&] { return launch_sweep(p, 0, us, inc, 0, 1, t, s); });
@@ -334,6 +333,9 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
     if (exact) {
       rc = timed(p, HD_TK_SWEEP_Z, s, [&] { return launch_sweep(p, 2, us, inc, 1, 0, t, s); });
       if (!rc && visc) rc = timed(p, HD_TK_PRIMS, s, [&] { return launch_prims(p, us, s); });
+    } else if (visc && xyx) {
+      // x/y ghost faces are strided: primitives of the whole ghosted box
+      rc = timed(p, HD_TK_PRIMS, s, [&] { return launch_prims(p, us, s); });
     } else if (visc && zx) {
       const int g = p->geo.g, nz = p->geo.n[2];
       rc = timed(p, HD_TK_PRIMS, s, [&] {

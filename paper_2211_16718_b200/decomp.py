@@ -5,16 +5,18 @@ decompose, default_dims, scatter, gather, parallel_advance, TimingReport,
 comm_fraction) with the reference's thread ranks + queues (decomp.py:146-268)
 replaced by torch.distributed over NCCL/NVLink:
 
-* blocks are split along z (dims = (1, 1, P)): each rank's z faces are
-  contiguous planes per variable, so the halo is sent straight out of the
-  state buffer with no pack kernel (SURVEY.md 8e);
+* any 3D block decomposition of the reference (decomp.py:66-103); the
+  default splits z only (dims = (1, 1, P)): z faces are contiguous planes per
+  variable, so the halo is sent straight out of the state buffer with no pack
+  kernel, and the x sweep never reads them; x and y faces of
+  split axes are packed into contiguous buffers;
 * the state face exchange of each RK stage is issued as one NCCL group
   (``batch_isend_irecv``) right after the previous stage's update kernel and
-  overlaps the x and y sweeps, which never read z ghosts; the z sweep waits
-  on it (``hd_stage_part`` HD_PART_LOCAL / HD_PART_HALO);
-* the viscous flux faces of the z-differentiated flux group (4 of the 9
-  symmetric flux fields, g planes) are exchanged while the y sweep runs, before
-  the z sweep that differentiates them;
+  overlaps the x sweep when x is not split (``hd_stage_part`` HD_PART_LOCAL /
+  HD_PART_HALO);
+* the viscous flux fields are exchanged along the axes that differentiate
+  them; the z group (4 of the 9 symmetric flux fields, g planes) while the y
+  sweep runs, before the z sweep that differentiates them;
 * the CFL signal and diagnostics are combined with ``all_reduce`` (MAX for
   signals, SUM for totals) on device tensors -- dt never leaves HBM.
 
@@ -153,141 +155,198 @@ def gather(locals_, layouts, spec: GridSpec) -> FieldSet:
     return out
 
 
+class _Pending:
+    """In-flight halo exchange: NCCL/gloo work handles plus the ghost slices
+    that receive the packed x/y faces once the work completes."""
+
+    def __init__(self, works=(), unpack=()):
+        self.works = list(works)
+        self.unpack = list(unpack)
+
+    def wait(self) -> None:
+        for w in self.works:
+            w.wait()
+        for dst, src in self.unpack:
+            dst.copy_(src)
+        self.works, self.unpack = [], []
+
+
 class DistHalo:
-    """Ghost synchronisation of one rank over torch.distributed (z split).
+    """Ghost synchronisation of one rank over torch.distributed.
 
     Drop-in for the reference's RankHalo (decomp.py:183-241): ``sync_fields``
-    and ``sync_scalars`` have the same meaning; ``exchange_z_async`` is the
-    overlapped form used by the fused march.  Works on CUDA tensors with the
-    NCCL backend and on CPU tensors with gloo (tests)."""
+    and ``sync_scalars`` have the same meaning (axes in x, y, z order, each
+    over the full ghosted extent of the others, so edges and corners match the
+    monolithic fill); ``exchange_async`` is the overlapped form used by the
+    fused march.  Any 3D block decomposition: an axis with one block wraps
+    locally (periodic), a split axis exchanges g planes with its two
+    neighbours.  z faces are contiguous per variable and are sent straight out
+    of the buffer; x and y faces are packed into contiguous buffers (one copy
+    kernel per face).  Works on CUDA tensors with NCCL and on CPU tensors with
+    gloo (tests)."""
 
     def __init__(self, layout: RankLayout, group=None):
-        if layout.dims[0] != 1 or layout.dims[1] != 1:
-            raise ConfigError(f"the GPU decomposition splits z only, got dims {layout.dims}")
         self.layout = layout
         self.group = group
-        self.periodic = (True, True, layout.dims[2] == 1)
+        self.periodic = tuple(layout.dims[d] == 1 for d in range(3))
+        self.split = tuple(d for d in range(3) if layout.dims[d] > 1)
         self.comm_seconds = 0.0
-        self.lo = layout.neighbor(2, -1)
-        self.hi = layout.neighbor(2, +1)
-        self._g_lo = self._g_hi = None
+        self.lo = tuple(layout.neighbor(d, -1) for d in range(3))
+        self.hi = tuple(layout.neighbor(d, +1) for d in range(3))
 
     def _peer(self, r: int) -> int:
         return r if self.group is None else dist.get_global_rank(self.group, r)
 
-    def _z_ops(self, buf: torch.Tensor, nfields: int, spec: GridSpec):
-        """P2P ops moving g z-planes of each field: my top interior planes to the
-        high neighbour's low ghosts, my bottom interior planes to the low
-        neighbour's high ghosts.  Issue order (send-hi, send-lo / recv-lo,
-        recv-hi) matches pairwise FIFO order even when lo == hi (2 ranks)."""
-        g = spec.ghost_width
-        nz = spec.n[2]
-        plane = spec.shape[1] * spec.shape[2]
-        slab = g * plane
-        npts = spec.total_points
-        ops = []
-        for f in range(nfields):
-            base = f * npts
-            top = buf[base + nz * plane: base + nz * plane + slab]          # planes [n, n+g)
-            bot = buf[base + g * plane: base + g * plane + slab]            # planes [g, 2g)
-            lo_ghost = buf[base: base + slab]                                # planes [0, g)
-            hi_ghost = buf[base + (nz + g) * plane: base + (nz + g) * plane + slab]
-            ops.append(dist.P2POp(dist.isend, top, self._peer(self.hi), self.group))
-            ops.append(dist.P2POp(dist.isend, bot, self._peer(self.lo), self.group))
-            ops.append(dist.P2POp(dist.irecv, lo_ghost, self._peer(self.lo), self.group))
-            ops.append(dist.P2POp(dist.irecv, hi_ghost, self._peer(self.hi), self.group))
-        return ops
+    def _axis_ops(self, v: torch.Tensor, fields, d: int, ops: list, unpack: list) -> None:
+        """P2P ops moving g planes of each listed field of ``v`` (nf, gz, gy, gx)
+        along axis d: my top interior planes to the high neighbour's low ghosts,
+        my bottom interior planes to the low neighbour's high ghosts.  Issue
+        order per field (send-hi, send-lo / recv-lo, recv-hi) matches pairwise
+        FIFO order even when lo == hi (2 blocks along d)."""
+        g = self.layout.spec.ghost_width
+        n = v.shape[3 - d] - 2 * g
+        dim = 3 - d  # tensor dim of axis d (fields, z, y, x)
+        hi, lo = self._peer(self.hi[d]), self._peer(self.lo[d])
+        for f in fields:
+            fv = v[f]
+            top, bot = fv.narrow(dim - 1, n, g), fv.narrow(dim - 1, g, g)
+            lo_ghost, hi_ghost = fv.narrow(dim - 1, 0, g), fv.narrow(dim - 1, n + g, g)
+            if d == 2:  # contiguous planes: no staging
+                ops.append(dist.P2POp(dist.isend, top, hi, self.group))
+                ops.append(dist.P2POp(dist.isend, bot, lo, self.group))
+                ops.append(dist.P2POp(dist.irecv, lo_ghost, lo, self.group))
+                ops.append(dist.P2POp(dist.irecv, hi_ghost, hi, self.group))
+            else:
+                r_lo, r_hi = torch.empty_like(lo_ghost, memory_format=torch.contiguous_format), \
+                    torch.empty_like(hi_ghost, memory_format=torch.contiguous_format)
+                ops.append(dist.P2POp(dist.isend, top.contiguous(), hi, self.group))
+                ops.append(dist.P2POp(dist.isend, bot.contiguous(), lo, self.group))
+                ops.append(dist.P2POp(dist.irecv, r_lo, lo, self.group))
+                ops.append(dist.P2POp(dist.irecv, r_hi, hi, self.group))
+                unpack += [(lo_ghost, r_lo), (hi_ghost, r_hi)]
 
-    def exchange_z_async(self, buf: torch.Tensor, nfields: int, spec: GridSpec):
-        if self.layout.dims[2] == 1:
-            return []
-        return dist.batch_isend_irecv(self._z_ops(buf, nfields, spec))
+    def exchange_async(self, buf: torch.Tensor, nfields: int, spec: GridSpec, axes=None,
+                       fields=None) -> _Pending:
+        """Exchange the split ``axes`` (default: all split axes) of fields
+        ``fields`` (default: all ``nfields``) of the flat buffer ``buf`` as one
+        NCCL group.  Faces of different axes go concurrently: the stencils are
+        axis-aligned, so no edge or corner ghost is ever read."""
+        axes = self.split if axes is None else tuple(d for d in axes if self.layout.dims[d] > 1)
+        if not axes:
+            return _Pending()
+        v = buf[: nfields * spec.total_points].view((nfields,) + spec.shape)
+        fields = range(nfields) if fields is None else fields
+        ops, unpack = [], []
+        for d in axes:
+            self._axis_ops(v, fields, d, ops, unpack)
+        return _Pending(dist.batch_isend_irecv(ops), unpack)
+
+    def exchange_z_async(self, buf: torch.Tensor, nfields: int, spec: GridSpec) -> _Pending:
+        return self.exchange_async(buf, nfields, spec, axes=(2,))
 
     @staticmethod
-    def wait(works) -> None:
-        for w in works:
-            w.wait()
+    def wait(pending) -> None:
+        if isinstance(pending, _Pending):
+            pending.wait()
+        else:
+            for w in pending:
+                w.wait()
 
-    def _wrap_xy(self, buf: torch.Tensor, nfields: int, spec: GridSpec) -> None:
-        """Local periodic wrap along x then y (grid.py:211-222), any device."""
+    @staticmethod
+    def _wrap(buf: torch.Tensor, nfields: int, spec: GridSpec, d: int) -> None:
+        """Local periodic wrap along axis d (grid.py:211-222), any device."""
         g = spec.ghost_width
-        nx, ny = spec.n[0], spec.n[1]
+        n = spec.n[d]
         v = buf.view((nfields,) + spec.shape)
-        v[..., :g] = v[..., nx:nx + g]
-        v[..., nx + g:] = v[..., g:2 * g]
-        v[..., :g, :] = v[..., ny:ny + g, :]
-        v[..., ny + g:, :] = v[..., g:2 * g, :]
+        dim = 3 - d
+        v.narrow(dim, 0, g).copy_(v.narrow(dim, n, g))
+        v.narrow(dim, n + g, g).copy_(v.narrow(dim, g, g))
 
-    def _wrap_z(self, buf, nfields, spec) -> None:
-        g = spec.ghost_width
-        nz = spec.n[2]
-        v = buf.view((nfields,) + spec.shape)
-        v[:, :g] = v[:, nz:nz + g]
-        v[:, nz + g:] = v[:, g:2 * g]
+    def _sync(self, flat: torch.Tensor, nfields: int, spec: GridSpec) -> None:
+        for d in range(3):
+            if self.layout.dims[d] == 1:
+                self._wrap(flat, nfields, spec, d)
+            else:
+                self.exchange_async(flat, nfields, spec, axes=(d,)).wait()
 
     def sync_fields(self, fields: FieldSet) -> FieldSet:
-        """x wrap, y wrap, z exchange (decomp.py:223-234): full-extent faces,
-        so edges and corners match the monolithic fill."""
+        """x, y, z in turn over full extents (decomp.py:223-234), so edges and
+        corners match the monolithic fill."""
         t0 = _time.perf_counter()
-        self._wrap_xy(fields.data, NVARS, fields.spec)
-        if self.layout.dims[2] == 1:
-            self._wrap_z(fields.data, NVARS, fields.spec)
-        else:
-            self.wait(self.exchange_z_async(fields.data, NVARS, fields.spec))
+        self._sync(fields.data, NVARS, fields.spec)
         self.comm_seconds += _time.perf_counter() - t0
         return fields
 
     def sync_scalars(self, arrays, n, g: int) -> None:
         spec = GridSpec(tuple(n), ghost_width=g)
         for arr in arrays:
-            flat = arr.reshape(-1)
-            self._wrap_xy(flat, 1, spec)
-            if self.layout.dims[2] == 1:
-                self._wrap_z(flat, 1, spec)
-            else:
-                self.wait(self.exchange_z_async(flat, 1, spec))
+            self._sync(arr.reshape(-1), 1, spec)
 
     # ---- fused march --------------------------------------------------------
     def advance(self, fields: FieldSet, gas: GasModel, tparams, weno_params: WenoParams,
                 delta: float, t0: float, observer, dt_provider, mode):
+        """The decomposed RK march.  Per stage (hd_stage_part):
+
+        * state faces of the stage input go out as one group; the LOCAL x sweep
+          overlaps them unless x itself is split (exact mode's LOCAL part also
+          sweeps y, so it waits for a y split too);
+        * HALO (ghost primitives + viscous fluxes) needs every state ghost;
+        * the viscous flux groups are exchanged along their own axes: the x and
+          y groups before MID (y sweep + D_x F_x + D_y F_y), the z group while
+          MID runs, before UPDATE (z sweep + D_z F_z + RK update)."""
         from .plan import get_plan
         from .timeint import _SCHEME_CODE, _as_device, _DeviceMarch
 
         fields = _as_device(fields)  # host (pinned) buffers are uploaded once
         spec = fields.spec
         plan = get_plan(spec, gas, weno_params, delta, mode, periodic=self.periodic)
+        exact = plan.mode == "exact"
         scheme = _SCHEME_CODE[tparams.scheme]
         nst = 3 if scheme == _lib.HD_SCHEME_RK3 else 4
         stage_buf = plan.fields(_lib.HD_BUF_STAGE, 2 * NVARS)  # ping-pong halves
         half = NVARS * spec.total_points
-        vflux_z = plan.fields(_lib.HD_BUF_VFLUX, 9)[5 * spec.total_points:]  # the z group
+        vflux = plan.fields(_lib.HD_BUF_VFLUX, 9)
         visc = gas.effective_mu != 0.0
         halo = self
+        local_waits = 0 in self.split or (exact and 1 in self.split)
+        pre_mid = tuple(d for d in (0, 1) if d in self.split)
 
         def stepper(u, dt_dev, tag):
-            plan.fill_ghosts(u, NVARS)  # x/y wrap of the step input (z: exchanged below)
+            plan.fill_ghosts(u, NVARS)  # periodic axes wrap locally; split axes exchanged below
             for s in range(nst):
                 us = u if s == 0 else stage_buf[((s - 1) % 2) * half: ((s - 1) % 2 + 1) * half]
-                works = halo.exchange_z_async(us, NVARS, spec)   # overlaps the x sweep
+                pend = halo.exchange_async(us, NVARS, spec)
+                if local_waits:
+                    pend.wait()
                 plan.stage_part(scheme, s, _lib.HD_PART_LOCAL, u, dt_dev, tag)
-                halo.wait(works)
+                pend.wait()
                 parts = _lib.HD_PART_HALO
                 if s == 0 and tag == 0:  # primitives of u not yet produced by an update
                     parts |= _lib.HD_PART_PRIMS
                 plan.stage_part(scheme, s, parts, u, dt_dev, tag)
-                works = halo.exchange_z_async(vflux_z, 4, spec) if visc else []
+                if visc and pre_mid:
+                    for d in pre_mid:
+                        halo.exchange_async(vflux, 9, spec, axes=(d,), fields=_VF_GROUP[d]).wait()
+                zpend = (halo.exchange_async(vflux, 9, spec, axes=(2,), fields=_VF_GROUP[2])
+                         if visc else _Pending())
                 plan.stage_part(scheme, s, _lib.HD_PART_MID, u, dt_dev, tag)  # overlaps it
-                halo.wait(works)
+                zpend.wait()
                 plan.stage_part(scheme, s, _lib.HD_PART_UPDATE, u, dt_dev, tag)
 
         def reducer(red):
-            if halo.layout.dims[2] > 1:
+            if self.split:
                 dist.all_reduce(red[0:3], op=dist.ReduceOp.MAX, group=halo.group)
                 dist.all_reduce(red[3:9], op=dist.ReduceOp.SUM, group=halo.group)
 
+        nblocks = self.layout.dims[0] * self.layout.dims[1] * self.layout.dims[2]
         march = _DeviceMarch(plan, fields, gas, tparams, t0, stepper=stepper, reducer=reducer,
-                             global_points=spec.interior_points * self.layout.dims[2])
+                             global_points=spec.interior_points * nblocks)
         return march.run(observer, dt_provider)
+
+
+# symmetric viscous flux fields (tau00 tau01 tau11 w0 w1 | tau02 tau12 tau22 w2) that
+# the divergence differentiates along each axis (hd_device.cuh vf_field)
+_VF_GROUP = ((0, 1, 5, 3), (1, 2, 6, 4), (5, 6, 7, 8))
 
 
 def parallel_advance(fields: FieldSet, gas: GasModel, tparams, weno_params: WenoParams = DEFAULT_PARAMS,

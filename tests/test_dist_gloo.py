@@ -48,13 +48,12 @@ def _wrapped(spec, body):
     return full
 
 
-def _worker(rank, world, port, n, q):
+def _worker(rank, world, port, n, q, dims):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         spec, body = _global_field(n)
-        dims = (1, 1, world)
         lay = hd.decompose(spec, dims)[rank]
         gfs = hd.FieldSet(spec, hd.Layout.COMPONENT_CONTIGUOUS,
                           torch.zeros(5 * spec.total_points, dtype=torch.float64))
@@ -64,15 +63,19 @@ def _worker(rank, world, port, n, q):
         halo.sync_fields(local)
         # expected: the monolithic wrapped field, cut to this rank's ghosted block
         full = _wrapped(spec, body)
-        oz = lay.offset[2]
-        lz = lay.local_n[2]
+        ox, oy, oz = lay.offset
+        lx, ly, lz = lay.local_n
         g = spec.ghost_width
-        want = full[:, oz: oz + lz + 2 * g]
+        # the wrapped global field is periodic, so the ghosted block is a periodic slice
+        zs = np.arange(oz - g, oz + lz + g) % spec.n[2] + g
+        ys = np.arange(oy - g, oy + ly + g) % spec.n[1] + g
+        xs = np.arange(ox - g, ox + lx + g) % spec.n[0] + g
+        want = full[:, zs][:, :, ys][:, :, :, xs]
         got = local.component_view().numpy()
         ok_fields = np.array_equal(got, want)
         # sync_scalars on one ghosted scalar (viscous.py:118 usage)
         arr = torch.zeros(lay.spec.shape, dtype=torch.float64)
-        arr[g:-g, g:-g, g:-g] = torch.from_numpy(body[4, oz: oz + lz])
+        arr[g:-g, g:-g, g:-g] = torch.from_numpy(body[4, oz: oz + lz, oy: oy + ly, ox: ox + lx])
         halo.sync_scalars([arr], lay.spec.n, g)
         ok_scalar = np.array_equal(arr.numpy(), want[4])
         # a reduction like the dt provider: MAX is exact on every rank
@@ -83,13 +86,19 @@ def _worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_z_slab_halo_matches_monolithic_wrap(world):
-    n = (6, 5, 4 * world)
+@pytest.mark.parametrize("dims", [(1, 1, 2), (1, 1, 4), (2, 1, 1), (1, 2, 1), (2, 2, 1), (1, 2, 2),
+                                  (2, 1, 2)])
+def test_block_halo_matches_monolithic_wrap(dims):
+    """Every 3D block decomposition (decomp.py:66-103): after sync_fields each
+    rank's ghosted block, edges and corners included, equals the periodic
+    slice of the monolithically wrapped field."""
+    world = dims[0] * dims[1] * dims[2]
+    n = (4 * dims[0] + 2, 4 * dims[1] + 1, 4 * dims[2])
+    n = tuple(n[d] if dims[d] == 1 else 4 * dims[d] for d in range(3))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q, dims)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]

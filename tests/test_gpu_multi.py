@@ -1,8 +1,9 @@
 """Decomposed runs on real GPUs (NCCL over NVLink), launched with torchrun from the test.
 
-Needs >= 2 visible GPUs; skipped otherwise.  A 2- and (if available) 4-rank
-z-slab run of config 1 (32^3 HIT, RK4, CFL 0.4, mu 0.006) must equal the
-single-GPU run bit-for-bit in exact mode (the reference's invariant,
+Needs >= 2 visible GPUs; skipped otherwise.  2- and (if available) 4-rank
+runs of config 1 (32^3 HIT, RK4, CFL 0.4, mu 0.006) over every block shape
+(z slabs, x and y splits, 2D splits) must equal the single-GPU run
+bit-for-bit in exact mode (the reference's invariant,
 pkg/tests/test_decomp.py:194-204) and to 1e-10 relative L2 in fast mode.
 """
 
@@ -29,27 +30,32 @@ dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["L
 mode = os.environ["HD_TEST_MODE"]
 spec = hd.GridSpec((32, 32, 32))
 ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
-res = hd.parallel_advance(ic, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=10),
-                          mode=mode)
-fin = res.fields.interior().cpu().numpy()
-if rank == 0:
-    print("RESULT " + json.dumps({"sha": hashlib.sha256(fin.tobytes()).hexdigest(), "t": res.t,
-                                  "l2": [float(np.sqrt((fin[v] ** 2).sum())) for v in range(5)]}))
+for dims in json.loads(os.environ["HD_TEST_DIMS"]):
+    res = hd.parallel_advance(ic, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=10),
+                              dims=tuple(dims), mode=mode)
+    fin = res.fields.interior().cpu().numpy()
+    if rank == 0:
+        print("RESULT " + json.dumps({"dims": dims, "sha": hashlib.sha256(fin.tobytes()).hexdigest(),
+                                      "t": res.t, "l2": [float(np.sqrt((fin[v] ** 2).sum())) for v in range(5)]}))
 dist.destroy_process_group()
 '''
+
+
+DIMS = {2: [(1, 1, 2), (2, 1, 1), (1, 2, 1)], 4: [(1, 1, 4), (2, 2, 1), (1, 2, 2), (2, 1, 2)]}
 
 
 def _run(world, mode, tmp_path):
     path = tmp_path / "pa.py"
     path.write_text(SCRIPT)
-    env = dict(os.environ, HD_ROOT=ROOT, HD_TEST_MODE=mode)
+    env = dict(os.environ, HD_ROOT=ROOT, HD_TEST_MODE=mode, HD_TEST_DIMS=json.dumps(DIMS[world]))
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                           f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
                           "--master-port=29533", str(path)], env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
-    line = [l for l in out.stdout.splitlines() if l.startswith("RESULT ")][0]
-    return json.loads(line[7:])
+    res = [json.loads(l[7:]) for l in out.stdout.splitlines() if l.startswith("RESULT ")]
+    assert [tuple(r["dims"]) for r in res] == DIMS[world]
+    return res
 
 
 @pytest.mark.parametrize("mode", ["exact", "fast"])
@@ -58,13 +64,13 @@ def test_decomposed_equals_single_gpu(tmp_path, traj32_golden, mode):
     if ngpu < 2:
         pytest.skip("needs >= 2 GPUs")
     for world in [w for w in (2, 4) if w <= ngpu]:
-        r = _run(world, mode, tmp_path)
-        if mode == "exact":
-            assert r["sha"] == traj32_golden["final_sha256"], world
-            assert r["t"] == traj32_golden["t"]
-        else:
-            import numpy as np
+        for r in _run(world, mode, tmp_path):
+            if mode == "exact":
+                assert r["sha"] == traj32_golden["final_sha256"], r["dims"]
+                assert r["t"] == traj32_golden["t"]
+            else:
+                import numpy as np
 
-            l2 = np.array(r["l2"])
-            want = np.array(traj32_golden["l2"])
-            assert np.all(np.abs(l2 - want) / want <= 1e-10), world
+                l2 = np.array(r["l2"])
+                want = np.array(traj32_golden["l2"])
+                assert np.all(np.abs(l2 - want) / want <= 1e-10), r["dims"]
