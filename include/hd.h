@@ -210,6 +210,18 @@ int64_t hd_launch_counter(void);
 /* FP64 FMA throughput probe: iters DFMA per thread on `out` (blocks x threads). */
 int hd_fp64_probe(double* out, int blocks, int threads, int iters, void* stream);
 
+/* Layout / traversal study (replaces kernels.py:292-329 bench_weights_lex /
+ * bench_weights_tiled, driven by bench.py:102-140 run_case).  `data` holds the
+ * (nx + 2 pad) * ny * nz points x 5 variables per `layout` (0 = INTERLEAVED,
+ * 1 = COMPONENT_CONTIGUOUS, grid.py Layout); the three WENO weights of every
+ * variable of every active point go to out[3 * (5 p + v) + 0..2] (point-major,
+ * so all combinations are bitwise comparable).  traversal 0 = lexicographic
+ * (one thread per active point, x fastest), 1 = (tx, ty) tiles per z plane;
+ * *wasted = idle lanes of the tiling (0 for lex).  Async on `stream`. */
+int hd_bench_weights(const double* data, int layout, int traversal, int nx, int ny, int nz, int pad,
+                     int tx, int ty, double eps, int power, double* out, int64_t* wasted,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

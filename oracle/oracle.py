@@ -15,6 +15,7 @@ buffers in the reference's own flat COMPONENT_CONTIGUOUS layout
 * :func:`rk3_step`         -- timeint.py:168-178
 * :func:`max_signal`       -- timeint.py:122-131
 * :func:`advance`          -- timeint.py:199-258 without diagnostics
+* :func:`bench_weights`    -- kernels.py:243-291 (layout-study weight kernel), numpy
 
 Parity of this oracle against the reference itself is pinned by
 ``tests/test_oracle_golden.py`` (fixtures from ``tests/golden/make_golden.py``).
@@ -236,3 +237,39 @@ def from_interior(body: np.ndarray, prob: Problem) -> np.ndarray:
     u = np.zeros(5 * prob.npts)
     interior(u, prob)[...] = body
     return fill_ghosts(u, prob)
+
+
+def bench_weights(values: np.ndarray, nx: int, ny: int, nz: int, pad: int = 2,
+                  eps: float = 1e-6, power: int = 2) -> np.ndarray:
+    """Point-major weights of the layout study (kernels.py:243-291) from the
+    canonical (points, 5) values: out[3 * (5 p + v) + 0..2] for the active
+    points, zero elsewhere.  numpy evaluates every binary op in IEEE double
+    without contraction, in the association order written below -- the same
+    as the numba kernel (pinned by tests/golden/bench_weights.npz)."""
+    px = nx + 2 * pad
+    npts = px * ny * nz
+    out = np.zeros((npts, 5, 3))
+    p = (np.arange(nz)[:, None, None] * ny + np.arange(ny)[None, :, None]) * px + pad + \
+        np.arange(nx)[None, None, :]
+    p = p.reshape(-1)
+    for v in range(5):
+        f0, f1, f2, f3, f4 = (values[p + s, v] for s in (-2, -1, 0, 1, 2))
+        t1 = (f0 - 2.0 * f1) + f2
+        s1 = (f0 - 4.0 * f1) + 3.0 * f2
+        b1 = (13.0 / 12.0) * (t1 * t1) + 0.25 * (s1 * s1)
+        t2 = (f1 - 2.0 * f2) + f3
+        s2 = f1 - f3
+        b2 = (13.0 / 12.0) * (t2 * t2) + 0.25 * (s2 * s2)
+        t3 = (f2 - 2.0 * f3) + f4
+        s3 = (3.0 * f2 - 4.0 * f3) + f4
+        b3 = (13.0 / 12.0) * (t3 * t3) + 0.25 * (s3 * s3)
+        d1, d2, d3 = eps + b1, eps + b2, eps + b3
+        e1, e2, e3 = d1, d2, d3
+        for _ in range(power - 1):
+            e1, e2, e3 = e1 * d1, e2 * d2, e3 * d3
+        a1, a2, a3 = 0.1 / e1, 0.6 / e2, 0.3 / e3
+        asum = (a1 + a2) + a3
+        out[p, v, 0] = a1 / asum
+        out[p, v, 1] = a2 / asum
+        out[p, v, 2] = a3 / asum
+    return out.reshape(-1)

@@ -37,7 +37,7 @@ EXPORTS = (
     "hd_plan_destroy", "hd_plan_buffer", "hd_plan_total_points", "hd_fill_ghosts",
     "hd_hyper_sweep", "hd_hyperbolic_rhs", "hd_parabolic_rhs", "hd_central_diff4", "hd_rhs",
     "hd_step", "hd_stage_part", "hd_reduce_state", "hd_set_dt", "hd_commit_time",
-    "hd_error_read", "hd_error_clear", "hd_fp64_probe", "hd_launch_counter", "hd_timer_enable",
+    "hd_error_read", "hd_error_clear", "hd_fp64_probe", "hd_bench_weights", "hd_launch_counter", "hd_timer_enable",
     "hd_timer_read",
 )
 # hd_timer_read kinds (HD_TK_*)
@@ -112,6 +112,8 @@ def load(require_cuda: bool = False):
             "hd_error_read": ([P, ctypes.POINTER(ctypes.c_uint64), P], i32),
             "hd_error_clear": ([P, P], i32),
             "hd_fp64_probe": ([P, i32, i32, i32, P], i32),
+            "hd_bench_weights": ([P, i32, i32, i32, i32, i32, i32, i32, i32, ctypes.c_double, i32, P,
+                                  ctypes.POINTER(ctypes.c_int64), P], i32),
             "hd_launch_counter": ([], i64),
             "hd_timer_enable": ([P, i32], i32),
             "hd_timer_read": ([P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), i32],

@@ -17,6 +17,10 @@ Fixtures (tests/golden/):
   traj16.npz    16^3 HIT IC, 10 RK4 steps at CFL 0.4, mu=0.006: per-step
                 dt, totals, max wavespeed and the final interior state;
                 3 RK3 steps for the TVD-RK3 stepper
+  bench_weights.npz  layout-study weight kernel (kernels.py:292-329 via
+                bench.py:102 run_case): outputs of the 4 layout x traversal
+                cases on a ragged (9, 5, 3) grid (all bitwise equal) and the
+                canonical values of bench.make_bench_values
   traj32.json   config 1 (32^3, RK4, CFL 0.4, mu=0.006, 10 steps): IC and
                 final SHA-256, per-variable L2, dts, KE per step
 """
@@ -168,7 +172,26 @@ def trajectory32():
     print(json.dumps(doc, indent=1))
 
 
+def bench_weights():
+    from hitdns import bench
+
+    shape = (9, 5, 3)
+    out = {"shape": np.array(shape), "values": bench.make_bench_values(shape)}
+    for layout in (hd.Layout.INTERLEAVED, hd.Layout.COMPONENT_CONTIGUOUS):
+        for trav in ("lex", "tiled"):
+            rec, w = bench.run_case(shape, layout, trav, repeats=1)
+            out[f"out_{int(layout)}_{trav}"] = w
+            out[f"wasted_{int(layout)}_{trav}"] = np.array(rec.wasted_lanes)
+    np.savez_compressed(os.path.join(OUT, "bench_weights.npz"), **out)
+
+
 if __name__ == "__main__":
+    import sys as _sys
+
+    if _sys.argv[1:] == ["bench_weights"]:
+        bench_weights()
+        raise SystemExit(0)
+    bench_weights()
     kernel_vectors()
     trajectory16()
     trajectory32()
