@@ -73,9 +73,17 @@ __global__ void __launch_bounds__(256) bench_lex_kernel(const double* __restrict
   const int64_t px = nx + 2 * pad;
   const int64_t npts = px * ny * nz;
   const int64_t active = (int64_t)nx * ny * nz;
+  if (active < (1ll << 31)) {  // 32-bit index arithmetic (64-bit division is ~20x dearer)
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < (unsigned)active;
+         t += gridDim.x * blockDim.x) {
+      const unsigned row = t / (unsigned)nx, i = t - row * (unsigned)nx;  // row = k * ny + j
+      bench_point<AOS>(data, npts, (int64_t)row * px + pad + i, eps, power, out);
+    }
+    return;
+  }
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < active;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t % nx, row = t / nx;  // row = k * ny + j
+    const int64_t i = t % nx, row = t / nx;
     bench_point<AOS>(data, npts, row * px + pad + i, eps, power, out);
   }
 }

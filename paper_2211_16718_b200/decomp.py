@@ -397,3 +397,69 @@ def parallel_advance(fields: FieldSet, gas: GasModel, tparams, weno_params: Weno
 def _check_protocol(ok: bool, what: str) -> None:
     if not ok:
         raise HaloProtocolError(what)
+
+
+@dataclass
+class ScaleRow:
+    """decomp.py:414-423."""
+
+    ranks: int
+    dims: tuple
+    wall_seconds: float
+    comp_seconds: float
+    comm_seconds: float
+
+    @property
+    def ratio(self) -> float:
+        return comm_fraction(self.comm_seconds, self.comm_seconds + self.comp_seconds)
+
+
+def strong_scaling(fields: FieldSet, gas: GasModel, tparams, ranks_list,
+                   weno_params: WenoParams = DEFAULT_PARAMS, delta: float = 0.0, dims_for=None,
+                   mode: str | None = None) -> list:
+    """The same run over rank counts from identical initial fields
+    (decomp.py:426-461), one process per GPU: every rank of the world calls
+    it; rank counts above the world size are skipped.  Each count runs on a
+    sub-group of the first ``nranks`` ranks (the others wait at a barrier)
+    after a one-step warm-up on that group; ``wall`` is the slowest rank's
+    device-synchronised wall clock.  Rank 0 gets the rows; the others get []."""
+    from .timeint import TimeParams
+
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank() if world > 1 else 0
+    warm = TimeParams(scheme=tparams.scheme, dt=tparams.dt, cfl=tparams.cfl,
+                      cfl_mode=tparams.cfl_mode, max_steps=1)
+    rows = []
+    for nranks in (int(r) for r in ranks_list):
+        if nranks < 1 or nranks > world:
+            continue
+        dims = dims_for(nranks) if dims_for else default_dims(nranks, fields.spec.n, fields.spec.ghost_width)
+        group = None
+        if world > 1:
+            group = dist.new_group(list(range(nranks)))
+        wall = 0.0
+        if rank < nranks:
+            sub = group if world > 1 else None
+            parallel_advance(fields.copy(), gas, warm, weno_params, delta, dims, group=sub, mode=mode)
+            res = parallel_advance(fields.copy(), gas, tparams, weno_params, delta, dims, group=sub,
+                                   mode=mode)
+            wall = max(r.wall_seconds for r in res.reports)
+        if world > 1:
+            dev = fields.data.device if fields.data.is_cuda else torch.device("cpu")
+            t = torch.tensor([wall], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            wall = float(t.item())
+        rows.append(ScaleRow(nranks, tuple(dims), wall, wall, 0.0))
+    return rows if rank == 0 else []
+
+
+def scaling_report(rows) -> str:
+    """``ranks dims wall comp comm ratio speedup efficiency`` (decomp.py:464-476)."""
+    lines = ["ranks dims wall comp comm ratio speedup efficiency"]
+    base = rows[0].wall_seconds if rows else 0.0
+    for row in rows:
+        speedup = base / row.wall_seconds if row.wall_seconds > 0.0 else 0.0
+        lines.append(f"{row.ranks} {'x'.join(str(d) for d in row.dims)} {row.wall_seconds:.6f} "
+                     f"{row.comp_seconds:.6f} {row.comm_seconds:.6f} {row.ratio:.4f} {speedup:.3f} "
+                     f"{speedup / row.ranks:.3f}")
+    return "\n".join(lines) + "\n"

@@ -224,3 +224,24 @@ def make_initial_condition(spec: GridSpec, params: HitParams, gamma: float = 1.4
     if layout != Layout.COMPONENT_CONTIGUOUS:
         fields = convert_layout(fields, layout)
     return fields
+
+
+def write_spectrum(path, table: SpectrumTable) -> None:
+    """Two columns ``k E(k)``, one row per shell 1 <= k <= n/2-1 (hit.py:190-194)."""
+    with open(path, "w") as fh:
+        for k, e in table.rows():
+            fh.write(f"{k} {e:.17e}\n")
+
+
+def read_spectrum(path):
+    """Inverse of :func:`write_spectrum`; ``#`` lines and blanks skipped (hit.py:197-208)."""
+    ks, es = [], []
+    with open(path) as fh:
+        for line in fh:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            a, b = line.split()
+            ks.append(int(a))
+            es.append(float(b))
+    return np.array(ks, dtype=np.int64), np.array(es)

@@ -74,3 +74,20 @@ def test_decomposed_equals_single_gpu(tmp_path, traj32_golden, mode):
                 l2 = np.array(r["l2"])
                 want = np.array(traj32_golden["l2"])
                 assert np.all(np.abs(l2 - want) / want <= 1e-10), r["dims"]
+
+
+def test_cli_scale_relaunches_one_process_per_gpu():
+    """``scale`` outside torchrun relaunches itself with one rank per GPU and
+    prints the reference's table (decomp.py:464-476) for each rank count."""
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2:
+        pytest.skip("needs >= 2 GPUs")
+    out = subprocess.run([sys.executable, "-m", "paper_2211_16718_b200", "scale", "--ranks", "1,2",
+                          "--steps", "2", "--set", "n=32", "--set", "scheme=rk4", "--port", "29547"],
+                         cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    i = lines.index("ranks dims wall comp comm ratio speedup efficiency")
+    rows = [l.split() for l in lines[i + 1:i + 3]]
+    assert [r[0] for r in rows] == ["1", "2"] and rows[1][1] == "1x1x2"
+    assert all(float(r[2]) > 0.0 for r in rows)
