@@ -73,4 +73,7 @@ def test_gpu_init_run_spectrum(tmp_path, traj32_golden):
     assert cli.main(["spectrum", "--in", out]) == 0
     ks, es = hd.read_spectrum(out + ".spectrum.txt")
     assert list(ks) == list(range(1, 16))
-    assert es.sum() == pytest.approx(traj32_golden["ke"][-1], rel=1e-9)
+    it = fields.interior()
+    table = hd.compute_spectrum(it[1] / it[0], it[2] / it[0], it[3] / it[0])
+    assert np.allclose(es, np.array([e for _, e in table.rows()]), rtol=1e-12, atol=0.0)
+    assert table.total() == pytest.approx(traj32_golden["ke"][-1], rel=1e-9)

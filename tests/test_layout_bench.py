@@ -8,7 +8,6 @@ reference's harness tests (pkg/tests/test_bench.py, test_acceptance.py:214-237).
 """
 
 import os
-import sys
 
 import numpy as np
 import pytest
@@ -19,8 +18,7 @@ from conftest import ROOT
 import paper_2211_16718_b200 as hd
 from paper_2211_16718_b200 import bench
 
-sys.path.insert(0, os.path.join(ROOT, "oracle"))
-import oracle  # noqa: E402
+from oracle import oracle  # noqa: E402  (test infrastructure only)
 
 GOLD = np.load(os.path.join(ROOT, "tests", "golden", "bench_weights.npz"))
 COMBOS = [(hd.Layout.INTERLEAVED, "lex"), (hd.Layout.INTERLEAVED, "tiled"),
