@@ -458,18 +458,18 @@ __device__ __forceinline__ double dmax_nan(double a, double b) {
 __global__ void __launch_bounds__(RED_THREADS) reduce_kernel(const double* __restrict__ u, Geo G,
                                                              double gamma, double* partial,
                                                              unsigned long long* err, int64_t tag) {
-  const int64_t nint = (int64_t)G.n[0] * G.n[1] * G.n[2];
   const int64_t np = G.npts;
   const double ih0 = G.h[0], ih1 = G.h[1], ih2 = G.h[2];
   double smax = -INFINITY, ssum = -INFINITY, wmax = -INFINITY;
   double sums[6] = {0, 0, 0, 0, 0, 0};
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nint;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(t % G.n[0]);
-    const int64_t r = t / G.n[0];
-    const int j = (int)(r % G.n[1]);
-    const int k = (int)(r / G.n[1]);
-    const int64_t q = G.idx(i, j, k);
+  // one warp per x row (lanes stride x: coalesced, no per-point index division)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t rows = (int64_t)G.n[1] * G.n[2];
+  const int64_t wstride = (int64_t)gridDim.x * (RED_THREADS / 32);
+  for (int64_t r = blockIdx.x * (int64_t)(RED_THREADS / 32) + warp; r < rows; r += wstride) {
+  const int64_t row0 = G.idx(0, (int)(r % G.n[1]), (int)(r / G.n[1]));
+  for (int i = lane; i < G.n[0]; i += 32) {
+    const int64_t q = row0 + i;
     const double rho = u[q], m1 = u[np + q], m2 = u[2 * np + q], m3 = u[3 * np + q],
                  E = u[4 * np + q];
     // physics.py:58-71 cons_to_prim (true division), 87-89 sound speed
@@ -491,9 +491,9 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_kernel(const double* __res
     sums[4] += E;
     sums[5] += 0.5 * ((v0 * v0 + v1 * v1) + v2 * v2);
   }
+  }
   // deterministic block tree: warp shuffles, then warp leaders in order
   __shared__ double sh[RED_THREADS / 32][9];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double vals[9] = {smax, ssum, wmax, sums[0], sums[1], sums[2], sums[3], sums[4], sums[5]};
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -538,8 +538,8 @@ __global__ void reduce_finish_kernel(const double* partial, int nblocks, double*
 
 int launch_reduce(const hd_plan* p, const double* u, double* out, int64_t tag, cudaStream_t s) {
   const Geo& G = p->geo;
-  const int64_t nint = (int64_t)G.n[0] * G.n[1] * G.n[2];
-  int blocks = (int)((nint + RED_THREADS - 1) / RED_THREADS);
+  const int64_t rows = (int64_t)G.n[1] * G.n[2];  // one warp per x row
+  int blocks = (int)((rows + RED_THREADS / 32 - 1) / (RED_THREADS / 32));
   if (blocks > RED_BLOCKS_MAX) blocks = RED_BLOCKS_MAX;
   double* partial = (double*)(p->ws + p->off[HD_BUF_RED]);
   unsigned long long* err = (unsigned long long*)(p->ws + p->off[HD_BUF_ERR]);

@@ -382,7 +382,11 @@ __device__ __forceinline__ void store_prim(double* prim, const Geo& G, int i, in
   store_point_images<4>(prim, G.npts, G.idx(i, j, k), nd, dl, pv);
 }
 
-template <int DIM, bool EXACT, int ROLE>
+// PW: WENO power fixed at compile time (2, the reference default), or 0 = read
+// at run time.  A run-time exponent loop inside each of the 18 reconstructions
+// of an interface splits the code into basic blocks the scheduler cannot
+// interleave; the fixed form lets the independent variables overlap.
+template <int DIM, bool EXACT, int ROLE, int PW>
 __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) sweep_kernel(const SweepArgs a) {
   constexpr bool SMEM_WINDOW = SweepCfg<DIM>::smem_window;
   int li, lj, lk;
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   const double* __restrict__ u = a.u + base;
   double* __restrict__ inc = a.inc + base;
   const double gm1 = a.ph.gm1, eps = a.ph.eps;
-  const int power = a.ph.power;
+  const int power = PW ? PW : a.ph.power;
 
   // Window in shared memory (SMEM_WINDOW): a 5-slot ring per thread, slot =
   // position mod 5, 9 values per point (u0..u4, f1..f4; f0 == u_{1+dim});
@@ -685,7 +689,7 @@ constexpr bool XOUT_STAGE = HD_XOUT_STAGE;
 constexpr bool XRING = XC <= 2;
 constexpr int XMINB = XRING ? HD_SWEEP_MIN_BLOCKS_YZ : HD_SWEEP_MIN_BLOCKS_X;
 
-template <bool EXACT>
+template <bool EXACT, int PW>
 __global__ void __launch_bounds__(SWEEP_THREADS, XMINB) sweep_x_staged_kernel(const SweepArgs a) {
   constexpr int WARPS = SWEEP_THREADS / 32;
   __shared__ double xin[WARPS][2][NV][32 * XS_PAD];
@@ -707,7 +711,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, XMINB) sweep_x_staged_kernel(co
   const int64_t sy = G.sy;
   const int64_t base = row0 + (int64_t)lane * sy;  // this lane's row
   const double gm1 = a.ph.gm1, eps = a.ph.eps;
-  const int power = a.ph.power;
+  const int power = PW ? PW : a.ph.power;
   const int p0 = c0 - 3;  // first position entering the window
 
   // chunk t holds positions p0 + XC t .. p0 + XC t + XC-1 of all 32 rows; lane l
@@ -869,7 +873,8 @@ static int launch_dim(const hd_plan* p, const SweepArgs& a, int nseg, cudaStream
   if (DIM == 0) grid = dim3((G.n[1] + 31) / 32, (G.n[2] + BY - 1) / BY, nseg);
   else if (DIM == 1) grid = dim3((G.n[0] + 31) / 32, (G.n[2] + BY - 1) / BY, nseg);
   else grid = dim3((G.n[0] + 31) / 32, (G.n[1] + BY - 1) / BY, nseg);
-  sweep_kernel<DIM, EXACT, ROLE><<<grid, block, 0, s>>>(a);
+  if (!EXACT && a.ph.power == 2) sweep_kernel<DIM, EXACT, ROLE, EXACT ? 0 : 2><<<grid, block, 0, s>>>(a);
+  else sweep_kernel<DIM, EXACT, ROLE, 0><<<grid, block, 0, s>>>(a);
   hd::count_launches(1);
   return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
 }
@@ -913,8 +918,9 @@ int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int ac
     constexpr int BY = SWEEP_THREADS / 32;
     const Geo& G = p->geo;
     dim3 block(32, BY, 1), grid(G.n[1] / 32, (G.n[2] + BY - 1) / BY, nseg);
-    if (exact) sweep_x_staged_kernel<true><<<grid, block, 0, s>>>(a);
-    else sweep_x_staged_kernel<false><<<grid, block, 0, s>>>(a);
+    if (exact) sweep_x_staged_kernel<true, 0><<<grid, block, 0, s>>>(a);
+    else if (a.ph.power == 2) sweep_x_staged_kernel<false, 2><<<grid, block, 0, s>>>(a);
+    else sweep_x_staged_kernel<false, 0><<<grid, block, 0, s>>>(a);
     hd::count_launches(1);
     return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
   }
