@@ -44,22 +44,22 @@ extern "C" {
 #define HD_SCHEME_RK4 4
 
 /* stage parts (hd_stage_part): one RK stage, split around the halo seam.
- * Call in this order; between LOCAL and PRIMS/HALO the z ghosts of the stage
- * input must arrive, between MID and UPDATE the z ghosts of the viscous z-flux
- * group (fields 5..8 of HD_BUF_VFLUX). */
-#define HD_PART_LOCAL 1   /* x sweep (exact: + y sweep): no z ghosts read */
-#define HD_PART_HALO 2    /* exact: z sweep + primitives; fast: exchanged-plane primitives;
-                             both: viscous fluxes */
+ * Call in this order; between LOCAL and HALO the exchanged ghosts of the stage
+ * input must arrive (LOCAL reads x ghosts only: a y/z exchange may still be in
+ * flight), before MID the x/y ghosts of the viscous flux groups they
+ * differentiate, before UPDATE the z ghosts of the z-flux group (fields 5..8
+ * of HD_BUF_VFLUX). */
+#define HD_PART_LOCAL 1   /* x sweep (exact: + y sweep) */
+#define HD_PART_HALO 2    /* exact: z sweep + primitives + viscous fluxes;
+                             fast: viscous fluxes from the state (primitives on the fly) */
 #define HD_PART_MID 4     /* fast: y sweep + D_x F_x + D_y F_y */
-#define HD_PART_UPDATE 8  /* fast: z sweep + D_z F_z + RK update + primitives of the new state;
+#define HD_PART_UPDATE 8  /* fast: z sweep + D_z F_z + RK update;
                              exact: viscous divergence + RK update */
 #define HD_PART_ALL 15
-#define HD_PART_PRIMS 16  /* fast: viscous primitives of the stage input (whole box); needed
-                             before HALO when the previous update did not produce them */
+#define HD_PART_PRIMS 16  /* accepted, no effect (ABI 1 compatibility) */
 
 /* hd_step flags */
-#define HD_STEP_PRIMS_VALID 1 /* HD_BUF_PRIM holds the primitives of u (the previous
-                                 hd_step on this plan ended with u): skip recomputing them */
+#define HD_STEP_PRIMS_VALID 1 /* accepted, no effect (ABI 1 compatibility) */
 
 /* workspace buffers (hd_plan_buffer) */
 #define HD_BUF_STAGE 0 /* 10 fields: RK stage states, ping-pong halves (stage s writes half s%2) */

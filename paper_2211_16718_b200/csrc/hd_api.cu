@@ -211,7 +211,7 @@ int hd_parabolic_rhs(hd_plan* p, const double* u, double* inc, void* stream) {
   if (p->phys.mu == 0.0) return HD_OK;  // viscous.py:72-73
   if (!parts_supported(p)) return HD_E_UNSUPPORTED;
   int rc = launch_prims(p, u, S(stream));
-  if (!rc) rc = launch_gradflux(p, S(stream));
+  if (!rc) rc = launch_gradflux(p, nullptr, S(stream));
   if (!rc) rc = launch_divergence(p, 7, inc, inc, 0, HD_SCHEME_RK4, 0, nullptr, nullptr, S(stream));
   return rc;
 }
@@ -312,45 +312,33 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   const int64_t t = tag * 8 + 1 + stage;  // slot 1..4: RK stage (0 = pre-step CFL, 7 = diagnostics)
   int rc = HD_OK;
   const bool exact = p->mode == HD_MODE_EXACT;
-  double* prim = visc ? buf(p, HD_BUF_PRIM) : nullptr;
   double* vflux = visc ? buf(p, HD_BUF_VFLUX) : nullptr;
-  const bool zx = !p->geo.periodic[2];  // z ghosts come from a halo exchange
-  const bool xyx = !p->geo.periodic[0] || !p->geo.periodic[1];  // so do x and/or y ghosts
   // LOCAL: sweeps that read no z ghosts (a z-halo exchange of `us` can be in flight)
   if (parts & HD_PART_LOCAL) {
     rc = timed(p, HD_TK_SWEEP_X, s, [&] { return launch_sweep(p, 0, us, inc, 0, 1, t, s); });
     if (!rc && exact)
       rc = timed(p, HD_TK_SWEEP_Y, s, [&] { return launch_sweep(p, 1, us, inc, 1, 0, t, s); });
   }
-  // PRIMS (fast): viscous primitives of the stage input over the whole box;
-  // otherwise they come from the previous stage's update kernel
-  if (!rc && (parts & HD_PART_PRIMS) && !exact && visc)
-    rc = timed(p, HD_TK_PRIMS, s, [&] { return launch_prims(p, us, s); });
-  // HALO (reads the z ghosts of `us`)
+  // PRIMS: kept for ABI compatibility; no kernel (the fast gradflux derives
+  // the primitives from the state itself, exact mode makes them in HALO)
+  // HALO (reads every ghost of `us`)
   //   exact: z sweep, primitives of the whole box, viscous fluxes
-  //   fast:  primitives of exchanged ghost planes, viscous fluxes
+  //   fast:  viscous fluxes straight from the state (primitives on the fly)
   if (!rc && (parts & HD_PART_HALO)) {
     if (exact) {
       rc = timed(p, HD_TK_SWEEP_Z, s, [&] { return launch_sweep(p, 2, us, inc, 1, 0, t, s); });
       if (!rc && visc) rc = timed(p, HD_TK_PRIMS, s, [&] { return launch_prims(p, us, s); });
-    } else if (visc && xyx) {
-      // x/y ghost faces are strided: primitives of the whole ghosted box
-      rc = timed(p, HD_TK_PRIMS, s, [&] { return launch_prims(p, us, s); });
-    } else if (visc && zx) {
-      const int g = p->geo.g, nz = p->geo.n[2];
-      rc = timed(p, HD_TK_PRIMS, s, [&] {
-        int r = launch_prims_planes(p, us, 0, g, s);
-        return r ? r : launch_prims_planes(p, us, nz + g, nz + 2 * g, s);
-      });
+      if (!rc && visc) rc = timed(p, HD_TK_GRADFLUX, s, [&] { return launch_gradflux(p, nullptr, s); });
+    } else if (visc) {
+      rc = timed(p, HD_TK_GRADFLUX, s, [&] { return launch_gradflux(p, us, s); });
     }
-    if (!rc && visc) rc = timed(p, HD_TK_GRADFLUX, s, [&] { return launch_gradflux(p, s); });
   }
   // MID (fast): y sweep + D_x F_x + D_y F_y (no z ghosts of the fluxes read)
   if (!rc && (parts & HD_PART_MID) && !exact)
     rc = timed(p, HD_TK_SWEEP_Y, s, [&] { return launch_sweep_visc(p, us, inc, vflux, t, s); });
   // UPDATE (reads the z ghosts of the viscous z-flux group)
   //   exact: divergence in the viscous.py:112-120 order + RK update
-  //   fast:  z sweep + D_z F_z + RK update + primitives of the new state
+  //   fast:  z sweep + D_z F_z + RK update
   if (!rc && (parts & HD_PART_UPDATE)) {
     if (!dt_dev) return HD_E_ARG;
     if (exact)
@@ -359,7 +347,7 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
       });
     else
       rc = timed(p, HD_TK_SWEEP_Z, s, [&] {
-        return launch_sweep_update(p, us, inc, vflux, prim, scheme, stage, u, dt_dev, t, s);
+        return launch_sweep_update(p, us, inc, vflux, nullptr, scheme, stage, u, dt_dev, t, s);
       });
   }
   return rc;
@@ -367,6 +355,7 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
 
 int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag, int flags,
             void* stream) {
+  (void)flags;  // HD_STEP_PRIMS_VALID: no effect since ABI 1
   if (!p || !u || !dt_dev) return HD_E_ARG;
   if (!p->ws) return HD_E_WORKSPACE;
   if (scheme != HD_SCHEME_RK3 && scheme != HD_SCHEME_RK4) return HD_E_ARG;
@@ -375,9 +364,7 @@ int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag
   // timeint.py:153: the rhs syncs the ghosts of its input first
   int rc = launch_fill_ghosts(p, u, 5, 7, S(stream));
   for (int st = 0; st < nstages(scheme) && !rc; ++st) {
-    int parts = HD_PART_ALL;
-    if (st == 0 && !(flags & HD_STEP_PRIMS_VALID)) parts |= HD_PART_PRIMS;
-    rc = hd_stage_part(p, scheme, st, parts, u, dt_dev, tag, stream);
+    rc = hd_stage_part(p, scheme, st, HD_PART_ALL, u, dt_dev, tag, stream);
   }
   return rc;
 }

@@ -209,10 +209,24 @@ __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict_
 constexpr int GZ_TX = 32, GZ_TY = 8, GZ_H = 2;
 constexpr int GZ_PX = GZ_TX + 2 * GZ_H, GZ_PY = GZ_TY + 2 * GZ_H;
 
-template <bool EXACT>
+// fast-mode viscous primitives (u, v, w, T) from the 5 conserved values (the
+// prims_kernel formula; viscous.py:80-81)
+__device__ __forceinline__ void prims_of(const double (&c)[5], double gamma, double gm1,
+                                         double (&pv)[4]) {
+  const double inv = frcp(c[0]);
+  pv[0] = c[1] * inv;
+  pv[1] = c[2] * inv;
+  pv[2] = c[3] * inv;
+  pv[3] = gamma * (gm1 * (c[4] - (0.5 * inv) * (c[1] * c[1] + c[2] * c[2] + c[3] * c[3]))) * inv;
+}
+
+// FROM_U (fast mode): `src` is the conserved state and every loaded point is
+// converted to primitives on the fly (no primitive fields in HBM); else `src`
+// holds the 4 primitive fields.
+template <bool EXACT, bool FROM_U>
 __global__ void __launch_bounds__(GZ_TX * GZ_TY, 2) gradflux_zm_kernel(
     const double* __restrict__ prim, double* __restrict__ vf, Geo G, double mu, double q_coef,
-    int zseg) {
+    int zseg, double gamma) {
   // two plane tiles (double-buffered: one barrier per plane); every load is
   // issued one plane before it is needed (z queue: plane k+3; ring: plane k+1)
   __shared__ double tile[2][4][GZ_PY][GZ_PX];
@@ -226,14 +240,32 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, 2) gradflux_zm_kernel(
 #pragma unroll
   for (int d = 0; d < 3; ++d) coef[d] = 1.0 / (12.0 * G.h[d]);
   // z queue: qz[f][w] = prims field f at plane k - 2 + w of this column
-  double qz[4][5], nq[4];
+  // raw loads (NF fields) are issued one plane ahead and converted when used
+  constexpr int NF = FROM_U ? 5 : 4;
+  double qz[4][5], nq[NF];
   const int64_t col = G.idx(i, j, 0);
+  const double gm1 = gamma - 1.0;
+  auto load = [&](int64_t q, double (&v)[NF]) {
 #pragma unroll
-  for (int w = 1; w < 5; ++w)
+    for (int f = 0; f < NF; ++f) v[f] = __ldg(prim + f * np + q);
+  };
+  auto prims = [&](const double (&v)[NF], double (&pv)[4]) {
+    if constexpr (FROM_U) {
+      prims_of(v, gamma, gm1, pv);
+    } else {
 #pragma unroll
-    for (int f = 0; f < 4; ++f) qz[f][w] = __ldg(prim + f * np + col + (int64_t)(k0 - 3 + w) * sz);
+      for (int f = 0; f < 4; ++f) pv[f] = v[f];
+    }
+  };
 #pragma unroll
-  for (int f = 0; f < 4; ++f) nq[f] = __ldg(prim + f * np + col + (int64_t)(k0 + 2) * sz);
+  for (int w = 1; w < 5; ++w) {
+    double v[NF], pv[4];
+    load(col + (int64_t)(k0 - 3 + w) * sz, v);
+    prims(v, pv);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) qz[f][w] = pv[f];
+  }
+  load(col + (int64_t)(k0 + 2) * sz, nq);
   // halo ring of the plane tile (minus the never-read corners): <= 1 point per thread
   const int r = ty * GZ_TX + tx;
   int px = 0, py = 0;
@@ -252,26 +284,24 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, 2) gradflux_zm_kernel(
     has_ring = !((px < GZ_H || px >= GZ_H + GZ_TX) && (py < GZ_H || py >= GZ_H + GZ_TY));
   }
   const int64_t rcol = G.idx(blockIdx.x * GZ_TX + px - GZ_H, blockIdx.y * GZ_TY + py - GZ_H, 0);
-  double rv[4];
-  if (has_ring)
-#pragma unroll
-    for (int f = 0; f < 4; ++f) rv[f] = __ldg(prim + f * np + rcol + (int64_t)k0 * sz);
+  double rv[NF];
+  if (has_ring) load(rcol + (int64_t)k0 * sz, rv);
   for (int k = k0; k < k1; ++k) {
     const int b = k & 1;
+    double pq[4], pr[4];
+    prims(nq, pq);
+    if (has_ring) prims(rv, pr);
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
 #pragma unroll
       for (int w = 0; w < 4; ++w) qz[f][w] = qz[f][w + 1];
-      qz[f][4] = nq[f];
+      qz[f][4] = pq[f];
       tile[b][f][ty + GZ_H][tx + GZ_H] = qz[f][2];
-      if (has_ring) tile[b][f][py][px] = rv[f];
+      if (has_ring) tile[b][f][py][px] = pr[f];
     }
     if (k + 1 < k1) {
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        nq[f] = __ldg(prim + f * np + col + (int64_t)(k + 3) * sz);
-        if (has_ring) rv[f] = __ldg(prim + f * np + rcol + (int64_t)(k + 1) * sz);
-      }
+      load(col + (int64_t)(k + 3) * sz, nq);
+      if (has_ring) load(rcol + (int64_t)(k + 1) * sz, rv);
     }
     __syncthreads();
     double gr[3][3], gT[3];
@@ -319,9 +349,10 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, 2) gradflux_zm_kernel(
 }
 
 
-int launch_gradflux(const hd_plan* p, cudaStream_t s) {
+int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s) {
   const Geo& G = p->geo;
   const double* prim = (const double*)(p->ws + p->off[HD_BUF_PRIM]);
+  const bool exact = p->mode == HD_MODE_EXACT;
   double* vf = (double*)(p->ws + p->off[HD_BUF_VFLUX]);
   const double mu = p->phys.mu;
   const double q_coef = (-mu) / ((p->phys.gamma - 1.0) * p->phys.prandtl);  // viscous.py:107
@@ -333,12 +364,19 @@ int launch_gradflux(const hd_plan* p, cudaStream_t s) {
     const int zseg = (G.n[2] + nseg - 1) / nseg;
     nseg = (G.n[2] + zseg - 1) / zseg;
     dim3 block(GZ_TX, GZ_TY, 1), grid(G.n[0] / GZ_TX, G.n[1] / GZ_TY, nseg);
-    if (p->mode == HD_MODE_EXACT)
-      gradflux_zm_kernel<true><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg);
+    const double gamma = p->phys.gamma;
+    if (exact)
+      gradflux_zm_kernel<true, false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma);
+    else if (u)
+      gradflux_zm_kernel<false, true><<<grid, block, 0, s>>>(u, vf, G, mu, q_coef, zseg, gamma);
     else
-      gradflux_zm_kernel<false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg);
+      gradflux_zm_kernel<false, false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma);
     hd::count_launches(1);
     return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+  }
+  if (u && !exact) {  // point-wise fallback reads primitives: make them first
+    const int rc = launch_prims(p, u, s);
+    if (rc) return rc;
   }
   dim3 block(32, 4, 1), grid((G.n[0] + 31) / 32, (G.n[1] + 3) / 4, G.n[2]);
   if (p->mode == HD_MODE_EXACT)

@@ -122,7 +122,9 @@ int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, co
 int launch_prims_planes(const hd_plan* p, const double* u, int z_lo, int z_hi, cudaStream_t s);
 int launch_fill_ghosts(const hd_plan* p, double* f, int nfields, int axis_mask, cudaStream_t s);
 int launch_prims(const hd_plan* p, const double* u, cudaStream_t s);
-int launch_gradflux(const hd_plan* p, cudaStream_t s);
+// viscous flux fields; fast mode with u != nullptr derives the primitives from
+// the conserved state u on the fly, else they are read from HD_BUF_PRIM
+int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s);
 // divergence (+ optional RK update).  dims_mask: which d's divergence to add;
 // update: 0 = store inc, else RK stage update with scheme/stage.
 int launch_divergence(const hd_plan* p, int dims_mask, const double* inc_in, double* inc_out,

@@ -290,7 +290,7 @@ class DistHalo:
         * state faces of the stage input go out as one group; the LOCAL x sweep
           overlaps them unless x itself is split (exact mode's LOCAL part also
           sweeps y, so it waits for a y split too);
-        * HALO (ghost primitives + viscous fluxes) needs every state ghost;
+        * HALO (viscous fluxes) needs every state ghost;
         * the viscous flux groups are exchanged along their own axes: the x and
           y groups before MID (y sweep + D_x F_x + D_y F_y), the z group while
           MID runs, before UPDATE (z sweep + D_z F_z + RK update)."""
@@ -320,10 +320,7 @@ class DistHalo:
                     pend.wait()
                 plan.stage_part(scheme, s, _lib.HD_PART_LOCAL, u, dt_dev, tag)
                 pend.wait()
-                parts = _lib.HD_PART_HALO
-                if s == 0 and tag == 0:  # primitives of u not yet produced by an update
-                    parts |= _lib.HD_PART_PRIMS
-                plan.stage_part(scheme, s, parts, u, dt_dev, tag)
+                plan.stage_part(scheme, s, _lib.HD_PART_HALO, u, dt_dev, tag)
                 if visc and pre_mid:
                     for d in pre_mid:
                         halo.exchange_async(vflux, 9, spec, axes=(d,), fields=_VF_GROUP[d]).wait()

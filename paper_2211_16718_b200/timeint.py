@@ -318,11 +318,8 @@ class _DeviceMarch:
         self.ctx[_lib.HD_CTX_T] = self.t0
         self.red = torch.empty(_lib.HD_RED_N, dtype=torch.float64, device=dev)
         self.scheme = _SCHEME_CODE[tparams.scheme]
-        # multi-rank drivers override how a step runs and how reductions combine.
-        # After the first step the viscous primitives of u are left in the plan
-        # by the last stage's update kernel (HD_STEP_PRIMS_VALID).
-        self.stepper = stepper or (lambda u, dt_dev, tag: plan.step(
-            self.scheme, u, dt_dev, tag, _lib.HD_STEP_PRIMS_VALID if tag > 0 else 0))
+        # multi-rank drivers override how a step runs and how reductions combine
+        self.stepper = stepper or (lambda u, dt_dev, tag: plan.step(self.scheme, u, dt_dev, tag, 0))
         self.reducer = reducer or (lambda red: None)
 
     def _reduce(self, tag: int) -> None:
