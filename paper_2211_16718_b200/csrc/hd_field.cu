@@ -493,11 +493,16 @@ __device__ __forceinline__ double dmax_nan(double a, double b) {
   return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(a, b);
 }
 
+// EXACT: the reference's true divisions and sqrt (dt bitwise equal to the
+// reference); fast: one reciprocal of rho and multiplications by 1/h (dt within
+// a few ulp)
+template <bool EXACT>
 __global__ void __launch_bounds__(RED_THREADS) reduce_kernel(const double* __restrict__ u, Geo G,
                                                              double gamma, double* partial,
                                                              unsigned long long* err, int64_t tag) {
   const int64_t np = G.npts;
   const double ih0 = G.h[0], ih1 = G.h[1], ih2 = G.h[2];
+  const double rh0 = 1.0 / G.h[0], rh1 = 1.0 / G.h[1], rh2 = 1.0 / G.h[2];
   double smax = -INFINITY, ssum = -INFINITY, wmax = -INFINITY;
   double sums[6] = {0, 0, 0, 0, 0, 0};
   // one warp per x row (lanes stride x: coalesced, no per-point index division)
@@ -511,14 +516,22 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_kernel(const double* __res
     const double rho = u[q], m1 = u[np + q], m2 = u[2 * np + q], m3 = u[3 * np + q],
                  E = u[4 * np + q];
     // physics.py:58-71 cons_to_prim (true division), 87-89 sound speed
-    const double v0 = xd(m1, rho), v1 = xd(m2, rho), v2 = xd(m3, rho);
-    const double kin = xm(xm(0.5, rho), xa(xa(xm(v0, v0), xm(v1, v1)), xm(v2, v2)));
-    const double p = xm(gamma - 1.0, xs(E, kin));
+    double v0, v1, v2, p, a, s0, s1, s2;
+    if constexpr (EXACT) {
+      v0 = xd(m1, rho), v1 = xd(m2, rho), v2 = xd(m3, rho);
+      const double kin = xm(xm(0.5, rho), xa(xa(xm(v0, v0), xm(v1, v1)), xm(v2, v2)));
+      p = xm(gamma - 1.0, xs(E, kin));
+      a = xsqrt(xd(xm(gamma, p), rho));
+      s0 = xd(xa(fabs(v0), a), ih0), s1 = xd(xa(fabs(v1), a), ih1), s2 = xd(xa(fabs(v2), a), ih2);
+    } else {
+      const double inv = frcp(rho);
+      v0 = m1 * inv, v1 = m2 * inv, v2 = m3 * inv;
+      p = (gamma - 1.0) * (E - (0.5 * inv) * (m1 * m1 + m2 * m2 + m3 * m3));
+      a = sqrt(gamma * p * inv);
+      s0 = (fabs(v0) + a) * rh0, s1 = (fabs(v1) + a) * rh1, s2 = (fabs(v2) + a) * rh2;
+    }
     if (!(rho > 0.0)) latch_error(err, tag, 1, q);
     else if (!(p > 0.0)) latch_error(err, tag, 2, q);
-    const double a = xsqrt(xd(xm(gamma, p), rho));
-    const double s0 = xd(xa(fabs(v0), a), ih0), s1 = xd(xa(fabs(v1), a), ih1),
-                 s2 = xd(xa(fabs(v2), a), ih2);
     smax = dmax_nan(smax, dmax_nan(dmax_nan(s0, s1), s2));
     ssum = dmax_nan(ssum, xa(xa(s0, s1), s2));
     wmax = dmax_nan(wmax, xa(dmax_nan(dmax_nan(fabs(v0), fabs(v1)), fabs(v2)), a));
@@ -581,7 +594,11 @@ int launch_reduce(const hd_plan* p, const double* u, double* out, int64_t tag, c
   if (blocks > RED_BLOCKS_MAX) blocks = RED_BLOCKS_MAX;
   double* partial = (double*)(p->ws + p->off[HD_BUF_RED]);
   unsigned long long* err = (unsigned long long*)(p->ws + p->off[HD_BUF_ERR]);
-  reduce_kernel<<<blocks, RED_THREADS, 0, s>>>(u, G, p->phys.gamma, partial, err, tag); hd::count_launches(1);
+  if (p->mode == HD_MODE_EXACT)
+    reduce_kernel<true><<<blocks, RED_THREADS, 0, s>>>(u, G, p->phys.gamma, partial, err, tag);
+  else
+    reduce_kernel<false><<<blocks, RED_THREADS, 0, s>>>(u, G, p->phys.gamma, partial, err, tag);
+  hd::count_launches(1);
   reduce_finish_kernel<<<1, 32, 0, s>>>(partial, blocks, out); hd::count_launches(1);
   return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
 }
