@@ -206,6 +206,12 @@ __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict_
 // a per-thread register queue of 5 planes (each prims value is loaded once per
 // column), the x/y stencils from a shared-memory plane tile with a 2-point halo.
 // Needs n_x % 32 == 0 and n_y % 8 == 0 (else gradflux_kernel).
+#ifndef HD_GZ_MINB
+#define HD_GZ_MINB 2
+#endif
+#ifndef HD_GZ_WAVES
+#define HD_GZ_WAVES 4
+#endif
 constexpr int GZ_TX = 32, GZ_TY = 8, GZ_H = 2;
 constexpr int GZ_PX = GZ_TX + 2 * GZ_H, GZ_PY = GZ_TY + 2 * GZ_H;
 
@@ -224,7 +230,7 @@ __device__ __forceinline__ void prims_of(const double (&c)[5], double gamma, dou
 // converted to primitives on the fly (no primitive fields in HBM); else `src`
 // holds the 4 primitive fields.
 template <bool EXACT, bool FROM_U>
-__global__ void __launch_bounds__(GZ_TX * GZ_TY, 2) gradflux_zm_kernel(
+__global__ void __launch_bounds__(GZ_TX * GZ_TY, HD_GZ_MINB) gradflux_zm_kernel(
     const double* __restrict__ prim, double* __restrict__ vf, Geo G, double mu, double q_coef,
     int zseg, double gamma) {
   // two plane tiles (double-buffered: one barrier per plane); every load is
@@ -359,7 +365,7 @@ int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s) {
   if (G.n[0] % GZ_TX == 0 && G.n[1] % GZ_TY == 0 && !getenv("HD_NO_GZ")) {
     // z segments: enough blocks for ~4 waves of 2 blocks per SM
     const int64_t cols = (int64_t)(G.n[0] / GZ_TX) * (G.n[1] / GZ_TY);
-    int nseg = (int)((p->sm_count * 2 * 4 + cols - 1) / cols);
+    int nseg = (int)((p->sm_count * HD_GZ_MINB * HD_GZ_WAVES + cols - 1) / cols);
     nseg = nseg < 1 ? 1 : (nseg > G.n[2] ? G.n[2] : nseg);
     const int zseg = (G.n[2] + nseg - 1) / nseg;
     nseg = (G.n[2] + zseg - 1) / zseg;
