@@ -116,6 +116,16 @@ class Plan:
         return self.buffer(_lib.HD_BUF_CTX, _lib.HD_CTX_N)
 
     @property
+    def err_key(self) -> torch.Tensor:
+        """The device error key (int64 view; -1 = none)."""
+        key = ("err", 1)
+        if key not in self._bufs:
+            ptr = self.L.hd_plan_buffer(self.h, _lib.HD_BUF_ERR)
+            off = ptr - self.ws.data_ptr()
+            self._bufs[key] = self.ws[off: off + 8].view(torch.int64)
+        return self._bufs[key]
+
+    @property
     def red(self) -> torch.Tensor:
         """Slot for the HD_RED_* results (after the partials)."""
         full = self.buffer(_lib.HD_BUF_RED, 2048 * 9 + 16)

@@ -18,6 +18,7 @@ kernel are raised as the reference's ``StepError(step, stage)`` /
 
 from __future__ import annotations
 
+import os
 import time as _time
 from dataclasses import dataclass, field
 
@@ -28,7 +29,7 @@ from . import _lib
 from .errors import InvalidStateError, StepError
 from .grid import FieldSet, GridSpec, Layout, PeriodicHalo
 from .physics import DEFAULT_PARAMS, GasModel, WenoParams
-from .plan import get_plan
+from .plan import error_from_key, get_plan
 from .upwind import hyperbolic_rhs
 from .viscous import parabolic_rhs
 
@@ -319,6 +320,7 @@ class _DeviceMarch:
         self.red = torch.empty(_lib.HD_RED_N, dtype=torch.float64, device=dev)
         self.scheme = _SCHEME_CODE[tparams.scheme]
         # multi-rank drivers override how a step runs and how reductions combine
+        self.own_stepper = stepper is None and reducer is None
         self.stepper = stepper or (lambda u, dt_dev, tag: plan.step(self.scheme, u, dt_dev, tag, 0))
         self.reducer = reducer or (lambda red: None)
 
@@ -326,7 +328,97 @@ class _DeviceMarch:
         self.plan.reduce(self.out.data, self.red, tag)
         self.reducer(self.red)
 
+    # steps per CUDA graph replay (the launch-bound small-grid path)
+    GRAPH_CHUNK = 8
+    # measured on B200 (tools/small_grid.py, 41 RK4 steps incl. capture): 32^3 0.52 -> 0.40
+    # ms/step with graphs; 64^3 0.57 -> 0.62 and 128^3 2.39 -> 2.58 (kernel time dominates
+    # there and the capture does not pay back)
+    GRAPH_MAX_POINTS = 48 ** 3
+
+    def _graph_ok(self, observer, dt_provider) -> bool:
+        tp = self.tp
+        env = os.environ.get("HD_NO_GRAPH")
+        if env not in (None, "") and env != "0":
+            return False
+        small = self.spec.interior_points <= self.GRAPH_MAX_POINTS or env == "0"
+        return (self.own_stepper and observer is None and dt_provider is None and tp.t_final is None
+                and tp.max_steps is not None and tp.max_steps >= 1 + 2 * self.GRAPH_CHUNK
+                and self.out.data.is_cuda and small)
+
+    def _one_step(self, k: int, tag: int, cfl_mode: int) -> None:
+        """Step k of the march: dt, the RK stages, time, diagnostics of the new state.
+        ``tag`` is the step number the kernels latch errors with."""
+        tp, plan = self.tp, self.plan
+        if tp.dt is not None:
+            plan.set_dt(None, 0, 0.0, tp.dt, -1.0, self.ctx, tag * 8)
+        else:
+            plan.set_dt(self.red, cfl_mode, tp.cfl, 0.0, -1.0, self.ctx, tag * 8)
+        self.stepper(self.out.data, self.ctx[_lib.HD_CTX_DT:], tag)
+        plan.commit_time(self.ctx)
+        self._reduce(tag * 8 + 7)  # diagnostics of the new state = next step's CFL signal
+
+    def _run_graph(self) -> AdvanceResult:
+        """max_steps without host synchronisation, the steps replayed from CUDA
+        graphs of GRAPH_CHUNK steps (one launch per chunk instead of ~23 per
+        step).  Step 0 runs eagerly (it also loads every kernel); the kernels of
+        a chunk latch errors with chunk-relative step tags, so the error key is
+        moved to a per-chunk slot after each replay and decoded with the chunk's
+        first step as the base (earliest step still wins)."""
+        tp, plan = self.tp, self.plan
+        plan.error_clear()
+        dev = self.out.data.device
+        cfl_mode = 1 if tp.cfl_mode == "sum" else 0
+        S = self.GRAPH_CHUNK
+        nsteps = tp.max_steps
+        nchunks = (nsteps - 1) // S
+        rows = torch.empty((nsteps, 2 + _lib.HD_RED_N), dtype=torch.float64, device=dev)
+        err = plan.err_key
+        slots = torch.full((nchunks + 1,), -1, dtype=torch.int64, device=dev)
+        wall0 = _time.perf_counter()
+
+        def record(k):
+            rows[k, 0:2] = self.ctx[0:2]
+            rows[k, 2:] = self.red
+
+        if tp.dt is None:
+            self._reduce(0)
+        self._one_step(0, 0, cfl_mode)
+        record(0)
+        slots[0] = err[0]
+        err.fill_(-1)
+        chunk_rows = torch.empty((S, 2 + _lib.HD_RED_N), dtype=torch.float64, device=dev)
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.graph(graph, stream=side):
+            for r in range(S):
+                self._one_step(1 + r, r, cfl_mode)
+                chunk_rows[r, 0:2] = self.ctx[0:2]
+                chunk_rows[r, 2:] = self.red
+        torch.cuda.current_stream(dev).wait_stream(side)
+        for c in range(nchunks):
+            graph.replay()
+            rows[1 + c * S: 1 + (c + 1) * S] = chunk_rows
+            slots[c + 1] = err[0]
+            err.fill_(-1)
+        for k in range(1 + nchunks * S, nsteps):
+            self._one_step(k, k, cfl_mode)
+            record(k)
+        keys = slots.cpu().tolist()
+        host_rows = rows.cpu().numpy()
+        del graph
+        for i, key in enumerate(keys):
+            if key != -1:
+                plan.error_clear()
+                raise error_from_key(key & (2 ** 64 - 1), self.spec, 0 if i == 0 else 1 + (i - 1) * S)
+        self._check(step_base=0)
+        per = (_time.perf_counter() - wall0) / nsteps
+        records = [_record(k + 1, host_rows[k], self.spec, per, self.points) for k in range(nsteps)]
+        return AdvanceResult(fields=self.out, t=float(host_rows[-1][0]), records=records)
+
     def run(self, observer=None, dt_provider=None) -> AdvanceResult:
+        if self._graph_ok(observer, dt_provider):
+            return self._run_graph()
         tp, plan = self.tp, self.plan
         plan.error_clear()
         cap = tp.max_steps if tp.max_steps is not None else 64
