@@ -306,7 +306,7 @@ constexpr int SWEEP_THREADS = 64;
 #define HD_SWEEP_MIN_BLOCKS_X 4
 #endif
 #ifndef HD_SWEEP_FLUX_WINDOW
-#define HD_SWEEP_FLUX_WINDOW 0
+#define HD_SWEEP_FLUX_WINDOW 1
 #endif
 // L1 prefetch of the divergence operands: measured slower (143.8 vs 140.3 ms/step
 // at 512^3) -- the prefetches compete for LSU issue and L1 with the loads that follow
@@ -413,9 +413,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   // The VISC/UPDATE roles append 4 columns: the viscous flux group F_dim
   // (differentiated along the sweep) at the same positions, so D_dim F_dim
   // reads each flux value from HBM once.
-  // (HD_SWEEP_FLUX_WINDOW, off by default: measured slower at 512^3 -- the
-  // larger ring leaves too little L1 for the other streams of the kernel;
-  // the default reads the stencil directly, operands prefetched into L1.)
+  // (HD_SWEEP_FLUX_WINDOW: 1 = y sweep only, the default -- 8.28 -> 8.06 ms at
+  // 512^3; the z sweep reads its stencil directly: with the window it spills
+  // at 168 registers and takes 9.9 -> 12.1 ms)
   constexpr bool VROLE = ROLE != ROLE_PLAIN;
   constexpr bool FWIN = VROLE && (HD_SWEEP_FLUX_WINDOW == 3 ||
                                   (HD_SWEEP_FLUX_WINDOW == 1 && ROLE == ROLE_VISC) ||
