@@ -306,7 +306,7 @@ constexpr int SWEEP_THREADS = 64;
 #define HD_SWEEP_MIN_BLOCKS_X 4
 #endif
 #ifndef HD_SWEEP_FLUX_WINDOW
-#define HD_SWEEP_FLUX_WINDOW 1
+#define HD_SWEEP_FLUX_WINDOW 3
 #endif
 // L1 prefetch of the divergence operands: measured slower (143.8 vs 140.3 ms/step
 // at 512^3) -- the prefetches compete for LSU issue and L1 with the loads that follow
@@ -316,9 +316,15 @@ constexpr int SWEEP_THREADS = 64;
 #ifndef HD_DIV_CPASYNC
 #define HD_DIV_CPASYNC 0
 #endif
+// z sweep (UPDATE role, flux window in the ring): 4 blocks/SM and up to 255
+// registers -- 9.7 -> 9.25 ms at 512^3 (6 blocks: spills; 4 without the window: 11.4)
+#ifndef HD_SWEEP_MIN_BLOCKS_Z
+#define HD_SWEEP_MIN_BLOCKS_Z 4
+#endif
 template <int DIM> struct SweepCfg {
   static constexpr bool smem_window = DIM != 0 && HD_SWEEP_SMEM_WINDOW_YZ;
-  static constexpr int min_blocks = DIM == 0 ? HD_SWEEP_MIN_BLOCKS_X : HD_SWEEP_MIN_BLOCKS_YZ;
+  static constexpr int min_blocks =
+      DIM == 0 ? HD_SWEEP_MIN_BLOCKS_X : (DIM == 1 ? HD_SWEEP_MIN_BLOCKS_YZ : HD_SWEEP_MIN_BLOCKS_Z);
 };
 
 // What a sweep does besides -dF/dx (the fast-mode stage pipeline, hd_api.cu):
@@ -413,9 +419,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   // The VISC/UPDATE roles append 4 columns: the viscous flux group F_dim
   // (differentiated along the sweep) at the same positions, so D_dim F_dim
   // reads each flux value from HBM once.
-  // (HD_SWEEP_FLUX_WINDOW: 1 = y sweep only, the default -- 8.28 -> 8.06 ms at
-  // 512^3; the z sweep reads its stencil directly: with the window it spills
-  // at 168 registers and takes 9.9 -> 12.1 ms)
+  // (HD_SWEEP_FLUX_WINDOW: 3 = both roles, the default -- y 8.28 -> 8.06 ms,
+  // z 9.7 -> 9.25 ms at 512^3 with the z sweep at 4 blocks/SM; 1 = y only,
+  // 2 = z only, 0 = stencil read directly from HBM/L1)
   constexpr bool VROLE = ROLE != ROLE_PLAIN;
   constexpr bool FWIN = VROLE && (HD_SWEEP_FLUX_WINDOW == 3 ||
                                   (HD_SWEEP_FLUX_WINDOW == 1 && ROLE == ROLE_VISC) ||
