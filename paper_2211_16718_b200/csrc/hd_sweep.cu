@@ -901,7 +901,10 @@ static SweepArgs make_args(const hd_plan* p, int dim, const double* u, double* i
   a.tag = tag;
   // segment length: enough independent lines to fill ~6 waves of 148 SMs x 256 threads
   const int64_t lines = (int64_t)G.n[0] * G.n[1] * G.n[2] / G.n[dim];
-  const int64_t target = (int64_t)p->sm_count * 256 * 6;
+#ifndef HD_SWEEP_WAVES
+#define HD_SWEEP_WAVES 6
+#endif
+  const int64_t target = (int64_t)p->sm_count * 256 * HD_SWEEP_WAVES;
   nseg = (int)((target + lines - 1) / lines);
   if (nseg < 1) nseg = 1;
   if (nseg > G.n[dim] / 8) nseg = G.n[dim] / 8 > 0 ? G.n[dim] / 8 : 1;
