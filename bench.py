@@ -213,6 +213,10 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's halo kernels on high-priority streams: their CTAs are scheduled ahead of
+        # the waiting sweep blocks, so the exchange overlaps instead of queueing behind
+        # (512^3 on 4 GPUs: 31.8 -> 31.1 ms/step)
+        os.environ.setdefault("TORCH_NCCL_HIGH_PRIORITY", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = args.n
     spec = hd.GridSpec((n, n, n))

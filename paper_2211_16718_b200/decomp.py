@@ -351,7 +351,9 @@ def parallel_advance(fields: FieldSet, gas: GasModel, tparams, weno_params: Weno
                      mode: str | None = None) -> ParallelResult:
     """Decomposed march; returns the gathered global state on every rank
     (decomp.py:328-407).  SPMD: every rank of ``group`` (default: the world)
-    calls it with the same global ``fields``; one rank per GPU."""
+    calls it with the same global ``fields``; one rank per GPU.  For the best
+    overlap of the halo with the sweeps, initialise NCCL with
+    ``TORCH_NCCL_HIGH_PRIORITY=1`` (bench.py and the CLI do)."""
     from .timeint import advance
 
     fields = fields if isinstance(fields, FieldSet) else FieldSet.from_numpy(fields)
