@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define HD_ABI_VERSION 1
+#define HD_ABI_VERSION 2
 
 /* status codes */
 #define HD_OK 0
@@ -70,7 +70,9 @@ extern "C" {
 #define HD_BUF_RED 5   /* reduction partials + results */
 #define HD_BUF_CTX 6   /* step context: t, dt, ... */
 #define HD_BUF_ERR 7   /* error key (uint64) */
-#define HD_NBUF 8
+#define HD_BUF_STATE 8 /* 5 fields: march state of a peer-attached plan (hd_peer_attach) */
+#define HD_BUF_SYNC 9  /* 8 uint64: peer flags (state from lo/hi, vflux from lo/hi), timeout word */
+#define HD_NBUF 10
 
 /* results of hd_reduce_state (doubles at HD_BUF_RED result slot) */
 #define HD_RED_SIGNAL_MAX 0
@@ -209,6 +211,38 @@ int64_t hd_launch_counter(void);
 /* ---- microbenchmark ---------------------------------------------------------- */
 /* FP64 FMA throughput probe: iters DFMA per thread on `out` (blocks x threads). */
 int hd_fp64_probe(double* out, int blocks, int threads, int iters, void* stream);
+
+/* ---- peer halo over NVLink (z slabs, one process per GPU) -------------------
+ * Replaces the NCCL face exchange of a z-slab decomposition (decomp.py:183-241
+ * RankHalo) for a plan whose z axis is not periodic: with the workspaces of the
+ * lower and upper z neighbours mapped into this process (hd_ipc_open of their
+ * hd_ipc_handle), every kernel that writes a stage state or a z-differentiated
+ * viscous flux stores the values of its g boundary planes straight into the
+ * neighbour's ghost planes (peer stores over NVLink; the same index deltas as
+ * the periodic images).  Requires the march state to live in HD_BUF_STATE.
+ * Protocol per RK stage with a counter v (1, 2, ...):
+ *   LOCAL; hd_peer_wait(STATE, v-1); HALO; hd_peer_signal(VFLUX, v); MID;
+ *   hd_peer_wait(VFLUX, v); UPDATE; hd_peer_signal(STATE, v)
+ * (the two halves of HD_BUF_STAGE make every write-after-read safe). */
+#define HD_PEER_STATE 0
+#define HD_PEER_VFLUX 1
+/* 64-byte IPC handle + byte offset of `ptr` inside its allocation. */
+int hd_ipc_handle(const void* ptr, void* handle64, int64_t* offset);
+/* Map a peer allocation (handle from hd_ipc_handle) into this process: *ptr =
+ * mapped base + offset. */
+int hd_ipc_open(const void* handle64, int64_t offset, void** ptr);
+/* Unmap (pass the pointer hd_ipc_open returned and its offset). */
+int hd_ipc_close(void* ptr, int64_t offset);
+/* lo_ws / hi_ws: the neighbours' workspaces as mapped here (may be equal: two
+ * ranks); NULL, NULL detaches.  Zeroes this plan's flags (call before any peer
+ * can signal, then barrier). */
+int hd_peer_attach(hd_plan* plan, void* lo_ws, void* hi_ws, void* stream);
+int hd_peer_signal(hd_plan* plan, int which, int64_t value, void* stream);
+/* Stream waits until both neighbours signalled >= value (spins at most
+ * ~30 s, then sets the timeout word of HD_BUF_SYNC and lets the stream go). */
+int hd_peer_wait(hd_plan* plan, int which, int64_t value, void* stream);
+/* 1 if a wait timed out since the attach. */
+int hd_peer_timed_out(hd_plan* plan, int* out, void* stream);
 
 /* Layout / traversal study (replaces kernels.py:292-329 bench_weights_lex /
  * bench_weights_tiled, driven by bench.py:102-140 run_case).  `data` holds the

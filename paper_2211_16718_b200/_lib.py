@@ -24,7 +24,8 @@ HD_SCHEME_RK4 = 4
 HD_PART_LOCAL, HD_PART_HALO, HD_PART_MID, HD_PART_UPDATE, HD_PART_ALL, HD_PART_PRIMS = 1, 2, 4, 8, 15, 16
 HD_STEP_PRIMS_VALID = 1
 (HD_BUF_STAGE, HD_BUF_ACC, HD_BUF_INC, HD_BUF_PRIM, HD_BUF_VFLUX, HD_BUF_RED, HD_BUF_CTX,
- HD_BUF_ERR) = range(8)
+ HD_BUF_ERR, HD_BUF_STATE, HD_BUF_SYNC) = range(10)
+HD_PEER_STATE, HD_PEER_VFLUX = 0, 1
 (HD_RED_SIGNAL_MAX, HD_RED_SIGNAL_SUM, HD_RED_WAVESPEED, HD_RED_MASS, HD_RED_MOMX, HD_RED_MOMY,
  HD_RED_MOMZ, HD_RED_ENERGY, HD_RED_KE) = range(9)
 HD_RED_N = 9
@@ -38,7 +39,8 @@ EXPORTS = (
     "hd_hyper_sweep", "hd_hyperbolic_rhs", "hd_parabolic_rhs", "hd_central_diff4", "hd_rhs",
     "hd_step", "hd_stage_part", "hd_reduce_state", "hd_set_dt", "hd_commit_time",
     "hd_error_read", "hd_error_clear", "hd_fp64_probe", "hd_bench_weights", "hd_launch_counter", "hd_timer_enable",
-    "hd_timer_read",
+    "hd_timer_read", "hd_ipc_handle", "hd_ipc_open", "hd_ipc_close", "hd_peer_attach", "hd_peer_signal",
+    "hd_peer_wait", "hd_peer_timed_out",
 )
 # hd_timer_read kinds (HD_TK_*)
 TIMER_KINDS = ("sweep_x", "sweep_y", "sweep_z", "gradflux", "prims", "divergence", "reduce")
@@ -115,6 +117,13 @@ def load(require_cuda: bool = False):
             "hd_bench_weights": ([P, i32, i32, i32, i32, i32, i32, i32, i32, ctypes.c_double, i32, P,
                                   ctypes.POINTER(ctypes.c_int64), P], i32),
             "hd_launch_counter": ([], i64),
+            "hd_ipc_handle": ([P, P, ctypes.POINTER(ctypes.c_int64)], i32),
+            "hd_ipc_open": ([P, i64, ctypes.POINTER(ctypes.c_void_p)], i32),
+            "hd_ipc_close": ([P, i64], i32),
+            "hd_peer_attach": ([P, P, P, P], i32),
+            "hd_peer_signal": ([P, i32, i64, P], i32),
+            "hd_peer_wait": ([P, i32, i64, P], i32),
+            "hd_peer_timed_out": ([P, ctypes.POINTER(ctypes.c_int), P], i32),
             "hd_timer_enable": ([P, i32], i32),
             "hd_timer_read": ([P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), i32],
                               i32),

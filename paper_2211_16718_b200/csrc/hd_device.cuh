@@ -55,9 +55,13 @@ __device__ __forceinline__ void store_with_images(double* f, const Geo& G, int i
       for (int a = 0; a < nx; ++a) f[G.idx(i + ox[a], j + oy[b], k + oz[c])] = v;
 }
 
+// axes whose face images kernels write: locally periodic axes, and z when the
+// images go to the z neighbours' ghost planes (peer stores, Geo::zpeer)
 __device__ __forceinline__ int periodic_mask(const Geo& G) {
-  return (G.periodic[0] ? 1 : 0) | (G.periodic[1] ? 2 : 0) | (G.periodic[2] ? 4 : 0);
+  return (G.periodic[0] ? 1 : 0) | (G.periodic[1] ? 2 : 0) | ((G.periodic[2] || G.zpeer) ? 4 : 0);
 }
+
+
 
 // v at interior (i,j,k) plus its face images along the axes in `mask`
 // (stencils here are axis-aligned: edges and corners are never read).
@@ -73,9 +77,9 @@ __device__ __forceinline__ void store_face_images(double* f, const Geo& G, int i
     if (j < g) f[G.idx(i, j + G.n[1], k)] = v;
     if (j >= G.n[1] - g) f[G.idx(i, j - G.n[1], k)] = v;
   }
-  if (mask & 4) {
-    if (k < g) f[G.idx(i, j, k + G.n[2])] = v;
-    if (k >= G.n[2] - g) f[G.idx(i, j, k - G.n[2])] = v;
+  if (mask & 4) {  // peer mode: into the z neighbours' ghost planes
+    if (k < g) f[G.idx(i, j, k + G.n[2]) + G.zpeer_lo] = v;
+    if (k >= G.n[2] - g) f[G.idx(i, j, k - G.n[2]) + G.zpeer_hi] = v;
   }
 }
 
@@ -191,22 +195,24 @@ __device__ __forceinline__ void rk_store(const RKArgs& r, const Geo& G, int i, i
 
 // fast-mode RK update with the base state and accumulator already in registers
 // Index deltas of the face images of interior point (i,j,k) along the axes in
-// `mask` (at most one per axis once n >= 2g); returns how many.
+// `mask` (at most one per axis once n >= 2g; z images land in the neighbours'
+// buffers in peer mode); returns how many.
 __device__ __forceinline__ int face_image_deltas(const Geo& G, int i, int j, int k, int mask,
-                                                 int64_t (&dl)[3]) {
+                                                 int64_t (&dl)[6]) {
   int nd = 0;
   const int g = G.g;
+  // both images of an axis when the block is thinner than 2g along it
   if (mask & 1) {
     if (i < g) dl[nd++] = G.n[0];
-    else if (i >= G.n[0] - g) dl[nd++] = -(int64_t)G.n[0];
+    if (i >= G.n[0] - g) dl[nd++] = -(int64_t)G.n[0];
   }
   if (mask & 2) {
     if (j < g) dl[nd++] = (int64_t)G.n[1] * G.sy;
-    else if (j >= G.n[1] - g) dl[nd++] = -(int64_t)G.n[1] * G.sy;
+    if (j >= G.n[1] - g) dl[nd++] = -(int64_t)G.n[1] * G.sy;
   }
   if (mask & 4) {
-    if (k < g) dl[nd++] = (int64_t)G.n[2] * G.sz;
-    else if (k >= G.n[2] - g) dl[nd++] = -(int64_t)G.n[2] * G.sz;
+    if (k < g) dl[nd++] = (int64_t)G.n[2] * G.sz + G.zpeer_lo;
+    if (k >= G.n[2] - g) dl[nd++] = -(int64_t)G.n[2] * G.sz + G.zpeer_hi;
   }
   return nd;
 }
@@ -214,7 +220,7 @@ __device__ __forceinline__ int face_image_deltas(const Geo& G, int i, int j, int
 // N fields (stride npts) at flat point q and its face images
 template <int N>
 __device__ __forceinline__ void store_point_images(double* f, int64_t np, int64_t q, int nd,
-                                                   const int64_t (&dl)[3], const double (&v)[N]) {
+                                                   const int64_t (&dl)[6], const double (&v)[N]) {
 #pragma unroll
   for (int c = 0; c < N; ++c) f[q + c * np] = v[c];
   for (int t = 0; t < nd; ++t)
@@ -237,7 +243,7 @@ __device__ __forceinline__ void rk_store_pre(const RKArgs& r, const Geo& G, int 
     if (r.wr_acc) r.acc[off] = fma(r.b0, acc[v], r.b1 * kv[v]);
     outv[v] = out;
   }
-  int64_t dl[3];
+  int64_t dl[6];
   const int nd = face_image_deltas(G, i, j, k, periodic_mask(G), dl);
   store_point_images<NV>(dst, G.npts, q, nd, dl, outv);
 }

@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict_
 #pragma unroll
   for (int f = 0; f < VF_N; ++f)
     store_face_images(vf + (int64_t)f * np, G, i, j, k, pm & vf_axes(f), val[f]);
+  if (G.zpeer && (k < G.g || k >= G.n[2] - G.g)) __threadfence_system();
 }
 
 // gradflux with z marching (blocks of 32 x 8 columns): the z stencil comes from
@@ -334,24 +335,36 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, HD_GZ_MINB) gradflux_zm_kernel(
     double val[VF_N];
     viscous_flux_point<EXACT>(gr, gT, vel, mu, q_coef, val);
     // each field gets face images only along the axes it is differentiated along
+    // (z images into the neighbours' ghost planes in peer mode)
     const int pm = periodic_mask(G);
     const int g = G.g;
     const int64_t q = G.idx(i, j, k);
-    const int64_t ax = (pm & 1) ? (i < g ? G.n[0] : (i >= G.n[0] - g ? -(int64_t)G.n[0] : 0)) : 0;
-    const int64_t ay = (pm & 2) ? (j < g ? (int64_t)G.n[1] * G.sy
-                                         : (j >= G.n[1] - g ? -(int64_t)G.n[1] * G.sy : 0)) : 0;
-    const int64_t az = (pm & 4) ? (k < g ? (int64_t)G.n[2] * sz
-                                         : (k >= G.n[2] - g ? -(int64_t)G.n[2] * sz : 0)) : 0;
+    const bool xl = (pm & 1) && i < g, xh = (pm & 1) && i >= G.n[0] - g;
+    const bool yl = (pm & 2) && j < g, yh = (pm & 2) && j >= G.n[1] - g;
+    const bool zl = (pm & 4) && k < g, zh = (pm & 4) && k >= G.n[2] - g;
+    const int64_t dy = (int64_t)G.n[1] * G.sy, dz = (int64_t)G.n[2] * sz;
 #pragma unroll
     for (int f = 0; f < VF_N; ++f) {
       double* F = vf + (int64_t)f * np + q;
-      F[0] = val[f];
+      const double v = val[f];
+      F[0] = v;
       const int axes = vf_axes(f);
-      if ((axes & 1) && ax) F[ax] = val[f];
-      if ((axes & 2) && ay) F[ay] = val[f];
-      if ((axes & 4) && az) F[az] = val[f];
+      if (axes & 1) {
+        if (xl) F[G.n[0]] = v;
+        if (xh) F[-G.n[0]] = v;
+      }
+      if (axes & 2) {
+        if (yl) F[dy] = v;
+        if (yh) F[-dy] = v;
+      }
+      if (axes & 4) {
+        if (zl) F[dz + G.zpeer_lo] = v;
+        if (zh) F[-dz + G.zpeer_hi] = v;
+      }
     }
   }
+  // peer stores performed before the kernel ends (only segments holding boundary planes)
+  if (G.zpeer && (k0 < G.g || k1 > G.n[2] - G.g)) __threadfence_system();
 }
 
 
@@ -411,6 +424,7 @@ __global__ void __launch_bounds__(128) divergence_kernel(const double* __restric
   add_viscous_divergence<EXACT>(vf, G, q, dmask, kv);
   if (update) {
     rk_store<EXACT>(r, G, i, j, k, kv);
+    if (G.zpeer && (k < G.g || k >= G.n[2] - G.g)) __threadfence_system();
   } else {
 #pragma unroll
     for (int v = 0; v < NV; ++v) inc_out[q + v * np] = kv[v];

@@ -383,7 +383,7 @@ __device__ __forceinline__ bool line_of(const SweepArgs& a, int& i, int& j, int&
 // along the locally periodic axes (the gradient stencils are axis-aligned).
 __device__ __forceinline__ void store_prim(double* prim, const Geo& G, int i, int j, int k,
                                            const double (&pv)[4]) {
-  int64_t dl[3];
+  int64_t dl[6];
   const int nd = face_image_deltas(G, i, j, k, periodic_mask(G), dl);
   store_point_images<4>(prim, G.npts, G.idx(i, j, k), nd, dl, pv);
 }
@@ -660,6 +660,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
       lf[v] = nf[v];
     }
   }
+  // peer stores (this line segment held boundary planes) performed before the kernel ends
+  if (ROLE == ROLE_UPDATE && DIM == 2 && G.zpeer && (c0 < G.g || c1 > nd - G.g))
+    __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------

@@ -27,6 +27,9 @@ single-GPU run bit-for-bit (the reference's invariant, test_decomp.py:194-204).
 
 from __future__ import annotations
 
+import ctypes
+import hashlib
+import os
 import time as _time
 from dataclasses import dataclass
 
@@ -300,6 +303,8 @@ class DistHalo:
         fields = _as_device(fields)  # host (pinned) buffers are uploaded once
         spec = fields.spec
         plan = get_plan(spec, gas, weno_params, delta, mode, periodic=self.periodic)
+        if self.peer_enabled(fields):
+            return self._advance_peer(plan, fields, gas, tparams, t0, observer, dt_provider)
         exact = plan.mode == "exact"
         scheme = _SCHEME_CODE[tparams.scheme]
         nst = 3 if scheme == _lib.HD_SCHEME_RK3 else 4
@@ -339,6 +344,127 @@ class DistHalo:
         march = _DeviceMarch(plan, fields, gas, tparams, t0, stepper=stepper, reducer=reducer,
                              global_points=spec.interior_points * nblocks)
         return march.run(observer, dt_provider)
+
+    def peer_enabled(self, fields: FieldSet) -> bool:
+        """z-slab blocks on CUDA: the halo goes over NVLink peer stores (hd_peer_*)
+        instead of NCCL, unless HD_PEER=0."""
+        return (self.split == (2,) and fields.data.is_cuda
+                and os.environ.get("HD_PEER", "1") not in ("0", ""))
+
+    def _advance_peer(self, plan, fields: FieldSet, gas: GasModel, tparams, t0, observer,
+                      dt_provider):
+        """The z-slab march with the halo fused into the producing kernels: the z
+        sweep's RK update and the flux kernel store their boundary planes into
+        the z neighbours' ghost planes over NVLink; per RK stage v
+
+            LOCAL; wait(state >= v-1); HALO; signal(vflux, v); MID;
+            wait(vflux >= v); UPDATE; signal(state, v)
+
+        (include/hd.h, hd_peer.cu).  The march state lives in the plan's
+        HD_BUF_STATE so the peers' images land at the same offsets."""
+        from .timeint import _SCHEME_CODE, _DeviceMarch
+
+        spec = fields.spec
+        scheme = _SCHEME_CODE[tparams.scheme]
+        nst = 3 if scheme == _lib.HD_SCHEME_RK3 else 4
+        visc = gas.effective_mu != 0.0
+        state = plan.fields(_lib.HD_BUF_STATE, NVARS)
+        state.copy_(fields.data)
+        local = FieldSet(spec, Layout.COMPONENT_CONTIGUOUS, state)
+        _PeerLink.get(self).attach(plan)
+        try:
+            self.exchange_async(state, NVARS, spec, axes=(2,)).wait()  # initial z ghosts
+            counter = [0]
+
+            def stepper(u, dt_dev, tag):
+                plan.fill_ghosts(u, NVARS)  # x/y wrap; z ghosts arrive as peer stores
+                for s in range(nst):
+                    v = counter[0] + 1
+                    plan.stage_part(scheme, s, _lib.HD_PART_LOCAL, u, dt_dev, tag)
+                    plan.peer_wait(_lib.HD_PEER_STATE, v - 1)
+                    plan.stage_part(scheme, s, _lib.HD_PART_HALO, u, dt_dev, tag)
+                    if visc:
+                        plan.peer_signal(_lib.HD_PEER_VFLUX, v)
+                    plan.stage_part(scheme, s, _lib.HD_PART_MID, u, dt_dev, tag)
+                    if visc:
+                        plan.peer_wait(_lib.HD_PEER_VFLUX, v)
+                    plan.stage_part(scheme, s, _lib.HD_PART_UPDATE, u, dt_dev, tag)
+                    plan.peer_signal(_lib.HD_PEER_STATE, v)
+                    counter[0] = v
+
+            def reducer(red):
+                dist.all_reduce(red[0:3], op=dist.ReduceOp.MAX, group=self.group)
+                dist.all_reduce(red[3:9], op=dist.ReduceOp.SUM, group=self.group)
+
+            march = _DeviceMarch(plan, local, gas, tparams, t0, stepper=stepper, reducer=reducer,
+                                 global_points=spec.interior_points * self.layout.dims[2],
+                                 copy=False)
+            res = march.run(observer, dt_provider)
+            timed_out = plan.peer_timed_out()
+        finally:
+            plan.peer_attach(None, None)  # the mapping stays cached (_PeerLink)
+        _check_protocol(not timed_out, "a z neighbour never signalled (peer halo timed out)")
+        res.fields = FieldSet(spec, Layout.COMPONENT_CONTIGUOUS, state.clone())
+        return res
+
+
+class _PeerLink:
+    """The z neighbours' plan workspaces mapped into this process (CUDA IPC).
+
+    Mappings are kept across marches (opening an IPC handle costs milliseconds):
+    each march all-gathers a 64-bit digest of every rank's (handle, offset) and
+    re-opens only what changed (a neighbour's plan was rebuilt)."""
+
+    _cache: dict = {}
+
+    def __init__(self, halo: "DistHalo"):
+        self.halo = halo
+        self.L = _lib.load()
+        self.digests = None
+        self.handles = None
+        self.opened = {}  # group rank -> (mapped pointer, offset)
+
+    @classmethod
+    def get(cls, halo: "DistHalo") -> "_PeerLink":
+        key = (id(halo.group), halo.layout.rank, halo.layout.dims)
+        link = cls._cache.get(key)
+        if link is None:
+            link = cls._cache[key] = cls(halo)
+        link.halo = halo
+        return link
+
+    def attach(self, plan) -> None:
+        halo = self.halo
+        world = dist.get_world_size(halo.group)
+        handle, off = plan.ipc_handle()
+        digest = int.from_bytes(hashlib.blake2b(handle + off.to_bytes(8, "little"),
+                                                digest_size=8).digest(), "little", signed=True)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        mine = torch.tensor([digest], dtype=torch.int64, device=dev)
+        alld = [torch.empty_like(mine) for _ in range(world)]
+        torch.cuda.synchronize()
+        dist.all_gather(alld, mine, group=halo.group)  # also: every rank finished its last march
+        digests = [int(t.item()) for t in alld]
+        if digests != self.digests:
+            allh = [None] * world
+            dist.all_gather_object(allh, (handle, off), group=halo.group)
+            self.release()
+            for r in {halo.lo[2], halo.hi[2]}:
+                h, o = allh[r]
+                ptr = ctypes.c_void_p()
+                _lib.check(self.L.hd_ipc_open(ctypes.create_string_buffer(h, 64), o,
+                                              ctypes.byref(ptr)), "hd_ipc_open")
+                self.opened[r] = (ptr.value, o)
+            self.digests = digests
+        plan.peer_attach(self.opened[halo.lo[2]][0], self.opened[halo.hi[2]][0])  # zeroes flags
+        torch.cuda.synchronize()
+        dist.barrier(group=halo.group)  # every rank's flags are zero before anyone signals
+
+    def release(self) -> None:
+        for ptr, off in self.opened.values():
+            self.L.hd_ipc_close(ctypes.c_void_p(ptr), off)
+        self.opened = {}
+        self.digests = None
 
 
 # symmetric viscous flux fields (tau00 tau01 tau11 w0 w1 | tau02 tau12 tau22 w2) that

@@ -183,6 +183,31 @@ class Plan:
         _lib.check(self.L.hd_timer_read(self.h, ms, cnt, n), "hd_timer_read")
         return {k: (ms[i], cnt[i]) for i, k in enumerate(_lib.TIMER_KINDS)}
 
+    # ---- peer halo over NVLink (z slabs) ----------------------------------
+    def ipc_handle(self) -> tuple:
+        """(64-byte IPC handle, offset) of this plan's workspace for a z neighbour."""
+        h = (ctypes.c_char * 64)()
+        off = ctypes.c_int64(0)
+        _lib.check(self.L.hd_ipc_handle(ctypes.c_void_p(self.ws.data_ptr() + self._ws_off), h,
+                                        ctypes.byref(off)), "hd_ipc_handle")
+        return bytes(h), int(off.value)
+
+    def peer_attach(self, lo_ptr: int | None, hi_ptr: int | None) -> None:
+        _lib.check(self.L.hd_peer_attach(self.h, ctypes.c_void_p(lo_ptr), ctypes.c_void_p(hi_ptr),
+                                         _stream_ptr()), "hd_peer_attach")
+
+    def peer_signal(self, which: int, value: int) -> None:
+        _lib.check(self.L.hd_peer_signal(self.h, which, value, _stream_ptr()), "hd_peer_signal")
+
+    def peer_wait(self, which: int, value: int) -> None:
+        _lib.check(self.L.hd_peer_wait(self.h, which, value, _stream_ptr()), "hd_peer_wait")
+
+    def peer_timed_out(self) -> bool:
+        out = ctypes.c_int(0)
+        _lib.check(self.L.hd_peer_timed_out(self.h, ctypes.byref(out), _stream_ptr()),
+                   "hd_peer_timed_out")
+        return bool(out.value)
+
     def error_key(self) -> int:
         key = ctypes.c_uint64(0)
         _lib.check(self.L.hd_error_read(self.h, ctypes.byref(key), _stream_ptr()), "hd_error_read")

@@ -304,7 +304,7 @@ class _DeviceMarch:
     """The fused single-device march shared by advance() and the decomposed driver."""
 
     def __init__(self, plan, fields: FieldSet, gas: GasModel, tparams: TimeParams, t0: float,
-                 stepper=None, reducer=None, global_points: int | None = None):
+                 stepper=None, reducer=None, global_points: int | None = None, copy: bool = True):
         self.plan = plan
         self.spec = fields.spec
         # interior points of the whole (possibly decomposed) domain: the KE mean
@@ -312,7 +312,7 @@ class _DeviceMarch:
         self.gas = gas
         self.tp = tparams
         self.t0 = float(t0)
-        self.out = fields.copy()
+        self.out = fields.copy() if copy else fields
         dev = self.out.data.device
         self.ctx = plan.ctx
         self.ctx.zero_()

@@ -44,17 +44,18 @@ dist.destroy_process_group()
 DIMS = {2: [(1, 1, 2), (2, 1, 1), (1, 2, 1)], 4: [(1, 1, 4), (2, 2, 1), (1, 2, 2), (2, 1, 2)]}
 
 
-def _run(world, mode, tmp_path):
+def _run(world, mode, tmp_path, dims=None, peer="1"):
     path = tmp_path / "pa.py"
     path.write_text(SCRIPT)
-    env = dict(os.environ, HD_ROOT=ROOT, HD_TEST_MODE=mode, HD_TEST_DIMS=json.dumps(DIMS[world]))
+    dims = DIMS[world] if dims is None else dims
+    env = dict(os.environ, HD_ROOT=ROOT, HD_TEST_MODE=mode, HD_TEST_DIMS=json.dumps(dims), HD_PEER=peer)
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                           f"--nproc-per-node={world}", "--master-addr=127.0.0.1",
                           "--master-port=29533", str(path)], env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     res = [json.loads(l[7:]) for l in out.stdout.splitlines() if l.startswith("RESULT ")]
-    assert [tuple(r["dims"]) for r in res] == DIMS[world]
+    assert [tuple(r["dims"]) for r in res] == [tuple(d) for d in dims]
     return res
 
 
@@ -74,6 +75,17 @@ def test_decomposed_equals_single_gpu(tmp_path, traj32_golden, mode):
                 l2 = np.array(r["l2"])
                 want = np.array(traj32_golden["l2"])
                 assert np.all(np.abs(l2 - want) / want <= 1e-10), r["dims"]
+
+
+def test_z_slab_nccl_halo_equals_single_gpu(tmp_path, traj32_golden):
+    """z slabs default to the NVLink peer-store halo (hd_peer_*); HD_PEER=0 keeps
+    the NCCL face exchange -- both must equal the single-GPU run bitwise."""
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 4 if ngpu >= 4 else 2
+    for r in _run(world, "exact", tmp_path, dims=[(1, 1, world)], peer="0"):
+        assert r["sha"] == traj32_golden["final_sha256"], r["dims"]
 
 
 def test_cli_scale_relaunches_one_process_per_gpu():
