@@ -342,7 +342,8 @@ class DistHalo:
 
         nblocks = self.layout.dims[0] * self.layout.dims[1] * self.layout.dims[2]
         march = _DeviceMarch(plan, fields, gas, tparams, t0, stepper=stepper, reducer=reducer,
-                             global_points=spec.interior_points * nblocks)
+                             global_points=spec.interior_points * nblocks,
+                             error_combine=lambda key: _combine_error_key(key, self.group))
         return march.run(observer, dt_provider)
 
     def peer_enabled(self, fields: FieldSet) -> bool:
@@ -398,14 +399,30 @@ class DistHalo:
 
             march = _DeviceMarch(plan, local, gas, tparams, t0, stepper=stepper, reducer=reducer,
                                  global_points=spec.interior_points * self.layout.dims[2],
-                                 copy=False)
+                                 copy=False,
+                                 error_combine=lambda key: _combine_error_key(key, self.group))
             res = march.run(observer, dt_provider)
-            timed_out = plan.peer_timed_out()
+            flag = torch.tensor([1 if plan.peer_timed_out() else 0], dtype=torch.int64,
+                                device=state.device)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
+            timed_out = bool(flag.item())
         finally:
             plan.peer_attach(None, None)  # the mapping stays cached (_PeerLink)
         _check_protocol(not timed_out, "a z neighbour never signalled (peer halo timed out)")
         res.fields = FieldSet(spec, Layout.COMPONENT_CONTIGUOUS, state.clone())
         return res
+
+
+def _combine_error_key(key: int, group) -> int:
+    """Earliest error over all ranks (0 = none): the key orders by step, stage,
+    code, then point, so MIN picks the error every rank must raise."""
+    none = (1 << 63) - 1
+    t = torch.tensor([key if key else none], dtype=torch.int64,
+                     device=torch.device("cuda", torch.cuda.current_device())
+                     if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    v = int(t.item())
+    return 0 if v == none else v
 
 
 class _PeerLink:

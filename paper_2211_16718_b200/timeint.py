@@ -304,7 +304,8 @@ class _DeviceMarch:
     """The fused single-device march shared by advance() and the decomposed driver."""
 
     def __init__(self, plan, fields: FieldSet, gas: GasModel, tparams: TimeParams, t0: float,
-                 stepper=None, reducer=None, global_points: int | None = None, copy: bool = True):
+                 stepper=None, reducer=None, global_points: int | None = None, copy: bool = True,
+                 error_combine=None):
         self.plan = plan
         self.spec = fields.spec
         # interior points of the whole (possibly decomposed) domain: the KE mean
@@ -323,6 +324,7 @@ class _DeviceMarch:
         self.own_stepper = stepper is None and reducer is None
         self.stepper = stepper or (lambda u, dt_dev, tag: plan.step(self.scheme, u, dt_dev, tag, 0))
         self.reducer = reducer or (lambda red: None)
+        self.error_combine = error_combine or (lambda key: key)
 
     def _reduce(self, tag: int) -> None:
         self.plan.reduce(self.out.data, self.red, tag)
@@ -475,7 +477,12 @@ class _DeviceMarch:
         return AdvanceResult(fields=self.out, t=t, records=records)
 
     def _check(self, step_base: int) -> None:
-        self.plan.raise_if_error(step_base=step_base)
+        """Raise the latched error; multi-rank drivers combine the keys first
+        (``error_combine``) so every rank raises the same error at the same step."""
+        key = self.error_combine(self.plan.error_key())
+        if key:
+            self.plan.error_clear()
+            raise error_from_key(key, self.spec, step_base)
 
 
 def write_step_log(path, records) -> None:

@@ -103,3 +103,50 @@ def test_cli_scale_relaunches_one_process_per_gpu():
     rows = [l.split() for l in lines[i + 1:i + 3]]
     assert [r[0] for r in rows] == ["1", "2"] and rows[1][1] == "1x1x2"
     assert all(float(r[2]) > 0.0 for r in rows)
+
+
+ERR_SCRIPT = r'''
+import json, os, sys
+sys.path.insert(0, os.environ["HD_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+import paper_2211_16718_b200 as hd
+rank = int(os.environ["RANK"])
+torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+n = 16
+spec = hd.GridSpec((n, n, n))
+fs = hd.FieldSet.zeros(spec, device="cpu")
+it = fs.interior()
+it[0] = 1.0
+it[4] = 2.5
+it[4, 13, 5, 6] = -1.0   # negative energy in the top z slab only
+out = {}
+for peer in ("1", "0"):
+    os.environ["HD_PEER"] = peer
+    try:
+        hd.parallel_advance(fs, hd.GasModel(), hd.TimeParams(scheme="rk4", dt=0.01, max_steps=3))
+        out[peer] = None
+    except hd.StepError as e:
+        out[peer] = [e.step, e.stage]
+print("RESULT " + json.dumps({"rank": rank, "err": out}), flush=True)
+dist.destroy_process_group()
+'''
+
+
+def test_step_error_raised_on_every_rank(tmp_path):
+    """An invalid state in one rank's block: every rank raises the same StepError
+    (error keys combined with MIN over ranks), none hangs in a collective."""
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2:
+        pytest.skip("needs >= 2 GPUs")
+    path = tmp_path / "err.py"
+    path.write_text(ERR_SCRIPT)
+    env = dict(os.environ, HD_ROOT=ROOT)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29541",
+                          str(path)], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = [json.loads(l[7:]) for l in out.stdout.splitlines() if l.startswith("RESULT ")]
+    assert len(res) == 2
+    for r in res:
+        assert r["err"]["1"] == [1, 0] and r["err"]["0"] == [1, 0], r
