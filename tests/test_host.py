@@ -135,3 +135,36 @@ def test_initial_condition_matches_reference_bits(traj32_golden):
     spec = hd.compute_spectrum(u.numpy(), v.numpy(), w.numpy())
     assert abs(spec.total() - traj32_golden["ke"][0]) < 1e-12
     assert abs(hd.viscosity_from_re_lambda(hd.HitParams()) - 0.006) < 1e-15
+
+
+def test_pointwise_physics_helpers():
+    """physics.py:58-255 utilities on tensors: round trip, fluxes, positivity errors."""
+    import paper_2211_16718_b200 as hd
+
+    rng = np.random.default_rng(11)
+    prim = np.stack([0.5 + rng.random(20), rng.standard_normal(20), rng.standard_normal(20),
+                     rng.standard_normal(20), 0.5 + rng.random(20)], axis=-1)
+    cons = hd.prim_to_cons(torch.from_numpy(prim), 1.4)
+    back = hd.cons_to_prim(cons, 1.4)
+    assert torch.allclose(back, torch.from_numpy(prim).to(back.device), rtol=1e-13, atol=1e-14)
+    a = hd.sound_speed(back, 1.4).cpu().numpy()
+    assert np.allclose(a, np.sqrt(1.4 * prim[:, 4] / prim[:, 0]), rtol=1e-14)
+    f = hd.convective_flux(cons, 1, 1.4).cpu().numpy()
+    c = cons.cpu().numpy()
+    assert np.allclose(f[:, 0], c[:, 2], rtol=1e-14)
+    assert np.allclose(f[:, 2], c[:, 2] * prim[:, 2] + prim[:, 4], rtol=1e-13)
+    assert np.allclose(hd.max_wavespeed(cons, 0, 1.4).cpu().numpy(), np.abs(prim[:, 1]) + a, rtol=1e-13)
+    g = torch.from_numpy(rng.standard_normal((4, 3, 3)))
+    tau = hd.viscous_stress(g, 0.1).cpu()
+    assert torch.allclose(tau, tau.transpose(-2, -1))
+    assert torch.allclose(tau.diagonal(dim1=-2, dim2=-1).sum(-1), torch.zeros(4, dtype=torch.float64), atol=1e-15)
+    bad = prim.copy()
+    bad[3, 0] = -1.0
+    with pytest.raises(hd.InvalidStateError):
+        hd.cons_to_prim(hd.prim_to_cons(torch.from_numpy(bad), 1.4), 1.4)
+    spec = hd.GridSpec((4, 4, 4))
+    fs = hd.FieldSet.zeros(spec, device="cpu")
+    fs.data.view(5, -1)[0] = 1.0
+    fs.data.view(5, -1)[4] = 2.5
+    rho, u, v, w, p = hd.decode_primitives(fs, 1.4)
+    assert float(p.min()) == pytest.approx(1.0) and float(u.abs().max()) == 0.0
