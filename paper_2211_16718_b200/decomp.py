@@ -303,7 +303,7 @@ class DistHalo:
         fields = _as_device(fields)  # host (pinned) buffers are uploaded once
         spec = fields.spec
         plan = get_plan(spec, gas, weno_params, delta, mode, periodic=self.periodic)
-        if self.peer_enabled(fields):
+        if self.peer_enabled(fields) and _PeerLink.get(self).attach(plan):
             return self._advance_peer(plan, fields, gas, tparams, t0, observer, dt_provider)
         exact = plan.mode == "exact"
         scheme = _SCHEME_CODE[tparams.scheme]
@@ -372,7 +372,6 @@ class DistHalo:
         state = plan.fields(_lib.HD_BUF_STATE, NVARS)
         state.copy_(fields.data)
         local = FieldSet(spec, Layout.COMPONENT_CONTIGUOUS, state)
-        _PeerLink.get(self).attach(plan)
         try:
             self.exchange_async(state, NVARS, spec, axes=(2,)).wait()  # initial z ghosts
             counter = [0]
@@ -450,7 +449,8 @@ class _PeerLink:
         link.halo = halo
         return link
 
-    def attach(self, plan) -> None:
+    def attach(self, plan) -> bool:
+        """Map/attach the neighbours; False on every rank if any rank cannot."""
         halo = self.halo
         world = dist.get_world_size(halo.group)
         handle, off = plan.ipc_handle()
@@ -466,16 +466,24 @@ class _PeerLink:
             allh = [None] * world
             dist.all_gather_object(allh, (handle, off), group=halo.group)
             self.release()
+            ok = 1
             for r in {halo.lo[2], halo.hi[2]}:
                 h, o = allh[r]
                 ptr = ctypes.c_void_p()
-                _lib.check(self.L.hd_ipc_open(ctypes.create_string_buffer(h, 64), o,
-                                              ctypes.byref(ptr)), "hd_ipc_open")
+                if self.L.hd_ipc_open(ctypes.create_string_buffer(h, 64), o, ctypes.byref(ptr)) != 0:
+                    ok = 0  # no IPC/P2P between these processes (e.g. no shared IPC namespace)
+                    break
                 self.opened[r] = (ptr.value, o)
+            flag = torch.tensor([ok], dtype=torch.int64, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=halo.group)
+            if not int(flag.item()):
+                self.release()
+                return False  # every rank falls back to the NCCL halo together
             self.digests = digests
         plan.peer_attach(self.opened[halo.lo[2]][0], self.opened[halo.hi[2]][0])  # zeroes flags
         torch.cuda.synchronize()
         dist.barrier(group=halo.group)  # every rank's flags are zero before anyone signals
+        return True
 
     def release(self) -> None:
         for ptr, off in self.opened.values():

@@ -128,7 +128,8 @@ for peer in ("1", "0"):
         out[peer] = None
     except hd.StepError as e:
         out[peer] = [e.step, e.stage]
-print("RESULT " + json.dumps({"rank": rank, "err": out}), flush=True)
+with open(os.path.join(os.environ["HD_OUT"], f"rank{rank}.json"), "w") as fh:
+    json.dump({"rank": rank, "err": out}, fh)
 dist.destroy_process_group()
 '''
 
@@ -141,12 +142,15 @@ def test_step_error_raised_on_every_rank(tmp_path):
         pytest.skip("needs >= 2 GPUs")
     path = tmp_path / "err.py"
     path.write_text(ERR_SCRIPT)
-    env = dict(os.environ, HD_ROOT=ROOT)
+    env = dict(os.environ, HD_ROOT=ROOT, HD_OUT=str(tmp_path))
     out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                           "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29541",
                           str(path)], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
-    res = [json.loads(l[7:]) for l in out.stdout.splitlines() if l.startswith("RESULT ")]
+    res = []
+    for r in range(2):
+        with open(tmp_path / f"rank{r}.json") as fh:
+            res.append(json.load(fh))
     assert len(res) == 2
     for r in res:
         assert r["err"]["1"] == [1, 0] and r["err"]["0"] == [1, 0], r
