@@ -119,8 +119,12 @@ def _synth_torch(n: int, params: HitParams, device):
     c[1] -= ky * kdot
     c[2] -= kz * kdot
     energy = 0.5 * (c.real ** 2 + c.imag ** 2).sum(dim=0)
-    raw = torch.bincount(shell.reshape(-1), weights=energy.reshape(-1), minlength=n // 2)
-    scale = torch.from_numpy(_shell_scale(raw.cpu().numpy(), n, params)).to(device)
+    # shell sums on the host: numpy's sequential bincount is reproducible bit-for-bit
+    # (torch.bincount with weights accumulates with atomics on the GPU: its order,
+    # hence the IC's last bits, would change from run to run and across processes)
+    raw = np.bincount(shell.reshape(-1).cpu().numpy(), weights=energy.reshape(-1).cpu().numpy(),
+                      minlength=n // 2)
+    scale = torch.from_numpy(_shell_scale(raw, n, params)).to(device)
     c *= scale[shell]
     del energy, kdot
     for a in range(3):

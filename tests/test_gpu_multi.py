@@ -154,3 +154,52 @@ def test_step_error_raised_on_every_rank(tmp_path):
     assert len(res) == 2
     for r in res:
         assert r["err"]["1"] == [1, 0] and r["err"]["0"] == [1, 0], r
+
+
+FULL_SCRIPT = r'''
+import hashlib, json, os, sys
+sys.path.insert(0, os.environ["HD_ROOT"])
+import torch, torch.distributed as dist
+import paper_2211_16718_b200 as hd
+rank = int(os.environ["RANK"])
+torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+spec = hd.GridSpec((512, 512, 512))
+ic = hd.make_initial_condition(spec, hd.HitParams(), backend="torch")
+res = hd.parallel_advance(ic, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=2),
+                          mode="exact")
+if rank == 0:
+    body = res.fields.interior().contiguous().cpu().numpy()
+    with open(os.path.join(os.environ["HD_OUT"], "full.json"), "w") as fh:
+        json.dump({"sha": hashlib.sha256(body.tobytes()).hexdigest(), "t": res.t}, fh)
+dist.destroy_process_group()
+'''
+
+
+def test_512_z_slabs_equal_single_gpu_bitwise(tmp_path):
+    """At the benchmark size (512^3, 2 RK4 steps, exact arithmetic) the 2-GPU z-slab
+    run with the NVLink peer-store halo equals the single-GPU run bit-for-bit."""
+    import hashlib
+
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import paper_2211_16718_b200 as hd
+
+    path = tmp_path / "full.py"
+    path.write_text(FULL_SCRIPT)
+    env = dict(os.environ, HD_ROOT=ROOT, HD_OUT=str(tmp_path))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29543",
+                          str(path)], env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    with open(tmp_path / "full.json") as fh:
+        multi = json.load(fh)
+    spec = hd.GridSpec((512, 512, 512))
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="torch", device="cuda:0")
+    res = hd.advance(ic, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=2),
+                     mode="exact")
+    body = res.fields.interior().contiguous().cpu().numpy()
+    hd.release_plans()
+    assert hashlib.sha256(body.tobytes()).hexdigest() == multi["sha"]
+    assert res.t == multi["t"]
