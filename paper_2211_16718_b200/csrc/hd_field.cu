@@ -213,7 +213,13 @@ __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict_
 #ifndef HD_GZ_WAVES
 #define HD_GZ_WAVES 4
 #endif
-constexpr int GZ_TX = 32, GZ_TY = 8, GZ_H = 2;
+#ifndef HD_GZ_TX
+#define HD_GZ_TX 32
+#endif
+#ifndef HD_GZ_TY
+#define HD_GZ_TY 8
+#endif
+constexpr int GZ_TX = HD_GZ_TX, GZ_TY = HD_GZ_TY, GZ_H = 2;
 constexpr int GZ_PX = GZ_TX + 2 * GZ_H, GZ_PY = GZ_TY + 2 * GZ_H;
 
 // fast-mode viscous primitives (u, v, w, T) from the 5 conserved values (the
