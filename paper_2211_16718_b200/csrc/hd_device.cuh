@@ -270,27 +270,4 @@ __device__ __forceinline__ void add_viscous_divergence(const double* __restrict_
   }
 }
 
-// L1 prefetch of every operand add_viscous_divergence reads at point q
-__device__ __forceinline__ void prefetch_divergence(const double* vf, const Geo& G, int64_t q,
-                                                    int dmask) {
-  const int64_t np = G.npts;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    if (!(dmask & (1 << d))) continue;
-    const int64_t st = G.stride(d);
-#pragma unroll
-    for (int row = 1; row < NV; ++row) {
-      const double* f = vf + (int64_t)vf_field(d, row) * np + q;
-      if (d == 0) {
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(f - 2));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(f + 2));
-      } else {
-#pragma unroll
-        for (int o = -2; o <= 2; ++o)
-          if (o) asm volatile("prefetch.global.L1 [%0];" ::"l"(f + o * st));
-      }
-    }
-  }
-}
-
 }  // namespace hd

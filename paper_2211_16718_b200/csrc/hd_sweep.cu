@@ -308,14 +308,6 @@ constexpr int SWEEP_THREADS = 64;
 #ifndef HD_SWEEP_FLUX_WINDOW
 #define HD_SWEEP_FLUX_WINDOW 3
 #endif
-// L1 prefetch of the divergence operands: measured slower (143.8 vs 140.3 ms/step
-// at 512^3) -- the prefetches compete for LSU issue and L1 with the loads that follow
-#ifndef HD_NO_DIV_PREFETCH
-#define HD_NO_DIV_PREFETCH 1
-#endif
-#ifndef HD_DIV_CPASYNC
-#define HD_DIV_CPASYNC 0
-#endif
 // z sweep (UPDATE role, flux window in the ring): 4 blocks/SM and up to 255
 // registers -- 9.7 -> 9.25 ms at 512^3 (6 blocks: spills; 4 without the window: 11.4)
 #ifndef HD_SWEEP_MIN_BLOCKS_Z
@@ -331,12 +323,12 @@ template <int DIM> struct SweepCfg {
 //   ROLE_PLAIN  inc (-)= dF/dx
 //   ROLE_VISC   y sweep: also adds the x and y viscous flux divergence
 //               D_x F_x + D_y F_y (viscous.py:119-120) of the cell it writes
-//   ROLE_UPDATE z sweep, last kernel of a stage: adds D_z F_z, feeds the finished
-//               increment to the RK stage update (timeint.py:168-193) instead of
-//               storing it, and stores the viscous primitives (u, v, w, T) of the
-//               new stage state (with face images) for the next stage's fluxes
-// The stencil operands of the divergence are pulled into L1 at the top of the
-// iteration that consumes them (prefetch.global.L1: no registers held).
+//   ROLE_UPDATE z sweep, last kernel of a stage: adds D_z F_z and feeds the
+//               finished increment to the RK stage update (timeint.py:168-193)
+//               instead of storing it; the new stage state goes out with its face
+//               images (into the z neighbours' ghost planes in peer mode)
+// The flux group differentiated along the sweep rides in the shared ring with the
+// window (one HBM read per value); the y sweep reads D_x's stencil directly.
 constexpr int ROLE_PLAIN = 0, ROLE_VISC = 1, ROLE_UPDATE = 2;
 
 struct SweepArgs {
@@ -430,12 +422,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   __shared__ double ring[SMEM_WINDOW ? 5 * RV * SWEEP_THREADS : 1];
   double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
   auto slot = [&](int m) -> double* { return mine + ((m + 5) % 5) * (RV * SWEEP_THREADS); };
-  // cp.async staging of the viscous-divergence operands (HD_DIV_CPASYNC)
-  constexpr bool DSTAGE = VROLE && !FWIN && HD_DIV_CPASYNC && !EXACT;
-  constexpr int DMASK = ROLE == ROLE_VISC ? 3 : 4;
-  constexpr int DN = ROLE == ROLE_VISC ? 32 : 16;
-  __shared__ double dstage[DSTAGE ? DN * SWEEP_THREADS : 1];
-  double* const dsb = dstage + threadIdx.y * 32 + threadIdx.x;
   double wu[5][NV], wf[5][NV];
   // viscous flux window: position p -> slot(p) columns 9..12; F(c+1) enters at
   // iteration c from fpre (loaded one iteration earlier)
@@ -515,33 +501,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
     }
     const bool wr = c > c0;
     double* q = inc + (int64_t)(c - 1) * sd;
-    if constexpr (VROLE && !FWIN && !HD_NO_DIV_PREFETCH && !DSTAGE) {
-      if (wr && a.vflux)
-        prefetch_divergence(a.vflux, G, base + (int64_t)(c - 1) * sd, ROLE == ROLE_VISC ? 3 : 4);
-    }
-    if constexpr (DSTAGE) {
-      // divergence operands of cell c-1 -> shared memory, consumed after the
-      // window's FP64 work (cp.async: no registers held meanwhile)
-      if (wr && a.vflux) {
-        const int64_t qc = base + (int64_t)(c - 1) * sd;
-        int o = 0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          if (!(DMASK & (1 << d))) continue;
-          const int64_t st = G.stride(d);
-#pragma unroll
-          for (int row = 1; row < NV; ++row) {
-            const double* f = a.vflux + (int64_t)vf_field(d, row) * np + qc;
-            cp_async8(dsb + (o + 0) * SWEEP_THREADS, f - 2 * st);
-            cp_async8(dsb + (o + 1) * SWEEP_THREADS, f - st);
-            cp_async8(dsb + (o + 2) * SWEEP_THREADS, f + st);
-            cp_async8(dsb + (o + 3) * SWEEP_THREADS, f + 2 * st);
-            o += 4;
-          }
-        }
-        cp_async_commit();
-      }
-    }
     // ROLE_UPDATE: the RK inputs of cell c-1 (base state, accumulator) are
     // loaded here, a full window of FP64 work before the update consumes them
     double ru0[NV], racc[NV];
@@ -607,21 +566,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
           for (int r = 0; r < 4; ++r) {
             const int o = r * SWEEP_THREADS;
             val[r + 1] += (8.0 * (p1[o] - m1[o]) + (m2[o] - p2[o])) * coef;
-          }
-        } else if (DSTAGE && a.vflux) {  // operands staged by cp.async at the top
-          cp_async_wait<0>();
-          int o = 0;
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            if (!(DMASK & (1 << d))) continue;
-            const double coef = 1.0 / (12.0 * G.h[d]);
-#pragma unroll
-            for (int row = 1; row < NV; ++row) {
-              val[row] += cd4v<false>(dsb[o * SWEEP_THREADS], dsb[(o + 1) * SWEEP_THREADS],
-                                      dsb[(o + 2) * SWEEP_THREADS], dsb[(o + 3) * SWEEP_THREADS],
-                                      coef);
-              o += 4;
-            }
           }
         } else if (VROLE && a.vflux) {  // direct stencil loads
           add_viscous_divergence<EXACT>(a.vflux, G, base + (int64_t)(c - 1) * sd,
