@@ -212,6 +212,11 @@ int64_t hd_launch_counter(void);
 /* FP64 FMA throughput probe: iters DFMA per thread on `out` (blocks x threads). */
 int hd_fp64_probe(double* out, int blocks, int threads, int iters, void* stream);
 
+/* Device pointer of the buffer that receives the output of RK stage `stage`
+ * (5 fields, ghosted; `u` for the last stage), i.e. the input of stage+1 --
+ * what a decomposed driver exchanges between the stage parts. */
+int hd_stage_buffer(hd_plan* plan, int scheme, int stage, double* u, void** out);
+
 /* ---- peer halo over NVLink (z slabs, one process per GPU) -------------------
  * Replaces the NCCL face exchange of a z-slab decomposition (decomp.py:183-241
  * RankHalo) for a plan whose z axis is not periodic: with the workspaces of the

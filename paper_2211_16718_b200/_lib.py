@@ -40,7 +40,7 @@ EXPORTS = (
     "hd_step", "hd_stage_part", "hd_reduce_state", "hd_set_dt", "hd_commit_time",
     "hd_error_read", "hd_error_clear", "hd_fp64_probe", "hd_bench_weights", "hd_launch_counter", "hd_timer_enable",
     "hd_timer_read", "hd_ipc_handle", "hd_ipc_open", "hd_ipc_close", "hd_peer_attach", "hd_peer_signal",
-    "hd_peer_wait", "hd_peer_timed_out",
+    "hd_peer_wait", "hd_peer_timed_out", "hd_stage_buffer",
 )
 # hd_timer_read kinds (HD_TK_*)
 TIMER_KINDS = ("sweep_x", "sweep_y", "sweep_z", "gradflux", "prims", "divergence", "reduce")
@@ -117,6 +117,7 @@ def load(require_cuda: bool = False):
             "hd_bench_weights": ([P, i32, i32, i32, i32, i32, i32, i32, i32, ctypes.c_double, i32, P,
                                   ctypes.POINTER(ctypes.c_int64), P], i32),
             "hd_launch_counter": ([], i64),
+            "hd_stage_buffer": ([P, i32, i32, P, ctypes.POINTER(ctypes.c_void_p)], i32),
             "hd_ipc_handle": ([P, P, ctypes.POINTER(ctypes.c_int64)], i32),
             "hd_ipc_open": ([P, i64, ctypes.POINTER(ctypes.c_void_p)], i32),
             "hd_ipc_close": ([P, i64], i32),

@@ -89,9 +89,9 @@ int nstages(int scheme) { return scheme == HD_SCHEME_RK3 ? 3 : 4; }
 
 void timer_free(void* t);  // defined with the Timer below
 
-// stage s > 0 reads the ping-pong half (s-1)%2 of the STAGE buffer (see make_rk)
-const double* stage_input(hd_plan* p, int stage, const double* u) {
-  return stage == 0 ? u : buf(p, HD_BUF_STAGE) + ((stage - 1) % 2) * NV * p->geo.npts;
+// stage s > 0 reads the output buffer of stage s-1 (hd_field.cu stage_buffer)
+const double* stage_input(hd_plan* p, int scheme, int stage, double* u) {
+  return stage == 0 ? u : stage_buffer(p, scheme, stage - 1, u);
 }
 
 }  // namespace
@@ -307,7 +307,7 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   if (!p->ws) return HD_E_WORKSPACE;
   if (stage < 0 || stage >= nstages(scheme)) return HD_E_ARG;
   cudaStream_t s = S(stream);
-  const double* us = stage_input(p, stage, u);
+  const double* us = stage_input(p, scheme, stage, u);
   double* inc = buf(p, HD_BUF_INC);
   const bool visc = p->phys.mu != 0.0;
   const int64_t t = tag * 8 + 1 + stage;  // slot 1..4: RK stage (0 = pre-step CFL, 7 = diagnostics)
@@ -370,6 +370,14 @@ int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag
     rc = hd_stage_part(p, scheme, st, HD_PART_ALL, u, dt_dev, tag, stream);
   }
   return rc;
+}
+
+int hd_stage_buffer(hd_plan* p, int scheme, int stage, double* u, void** out) {
+  if (!p || !u || !out || (scheme != HD_SCHEME_RK3 && scheme != HD_SCHEME_RK4)) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  if (stage < 0 || stage >= nstages(scheme)) return HD_E_ARG;
+  *out = stage_buffer(p, scheme, stage, u);
+  return HD_OK;
 }
 
 int hd_reduce_state(hd_plan* p, const double* u, double* out, int64_t tag, void* stream) {

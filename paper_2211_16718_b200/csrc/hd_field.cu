@@ -437,18 +437,22 @@ __global__ void __launch_bounds__(128) divergence_kernel(const double* __restric
   }
 }
 
+// Stage states ping-pong between the two halves of the STAGE buffer so a fused
+// sweep never overwrites points other threads still read: stage s reads half
+// (s-1)%2 (u for s = 0) and writes half s%2; the last stage writes u.
+double* stage_buffer(const hd_plan* p, int scheme, int stage, double* u) {
+  const int last = (scheme == HD_SCHEME_RK3 ? 3 : 4) - 1;
+  if (stage >= last) return u;
+  return (double*)(p->ws + p->off[HD_BUF_STAGE]) + (stage % 2) * NV * p->geo.npts;
+}
+
 RKArgs make_rk(const hd_plan* p, int scheme, int stage, double* u, const double* dt_dev) {
   RKArgs r;
   r.scheme = scheme;
   r.stage = stage;
   r.u = u;
-  // stage states ping-pong between the two halves of the STAGE buffer so a
-  // fused sweep never overwrites points other threads still read:
-  // stage s reads half (s-1)%2 (u for s = 0) and writes half s%2
-  double* st = (double*)(p->ws + p->off[HD_BUF_STAGE]);
-  const int64_t nf = NV * p->geo.npts;
-  r.stage_in = stage == 0 ? u : st + ((stage - 1) % 2) * nf;
-  r.stage_out = st + (stage % 2) * nf;
+  r.stage_in = stage == 0 ? u : stage_buffer(p, scheme, stage - 1, u);
+  r.stage_out = stage_buffer(p, scheme, stage, u);
   r.acc = (double*)(p->ws + p->off[HD_BUF_ACC]);
   r.dt = dt_dev;
   // fast-mode coefficients of the same tableaux (timeint.py:168-193)

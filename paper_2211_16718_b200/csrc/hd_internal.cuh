@@ -139,4 +139,6 @@ int launch_divergence(const hd_plan* p, int dims_mask, const double* inc_in, dou
 int launch_rk_update(const hd_plan* p, const double* inc, int scheme, int stage, double* u,
                      const double* dt_dev, cudaStream_t s);
 int launch_reduce(const hd_plan* p, const double* u, double* out, int64_t tag, cudaStream_t s);
+// the buffer holding the output of RK stage `stage` (u for the last one; hd_field.cu)
+double* stage_buffer(const hd_plan* p, int scheme, int stage, double* u);
 }  // namespace hd

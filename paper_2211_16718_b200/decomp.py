@@ -308,8 +308,6 @@ class DistHalo:
         exact = plan.mode == "exact"
         scheme = _SCHEME_CODE[tparams.scheme]
         nst = 3 if scheme == _lib.HD_SCHEME_RK3 else 4
-        stage_buf = plan.fields(_lib.HD_BUF_STAGE, 2 * NVARS)  # ping-pong halves
-        half = NVARS * spec.total_points
         vflux = plan.fields(_lib.HD_BUF_VFLUX, 9)
         visc = gas.effective_mu != 0.0
         halo = self
@@ -319,7 +317,7 @@ class DistHalo:
         def stepper(u, dt_dev, tag):
             plan.fill_ghosts(u, NVARS)  # periodic axes wrap locally; split axes exchanged below
             for s in range(nst):
-                us = u if s == 0 else stage_buf[((s - 1) % 2) * half: ((s - 1) % 2 + 1) * half]
+                us = plan.stage_input(scheme, s, u)
                 pend = halo.exchange_async(us, NVARS, spec)
                 if local_waits:
                     pend.wait()

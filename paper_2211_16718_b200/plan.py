@@ -183,6 +183,19 @@ class Plan:
         _lib.check(self.L.hd_timer_read(self.h, ms, cnt, n), "hd_timer_read")
         return {k: (ms[i], cnt[i]) for i, k in enumerate(_lib.TIMER_KINDS)}
 
+    def stage_input(self, scheme: int, stage: int, u: torch.Tensor) -> torch.Tensor:
+        """The 5-field buffer RK stage ``stage`` reads (``u`` for stage 0)."""
+        if stage == 0:
+            return u
+        out = ctypes.c_void_p()
+        _lib.check(self.L.hd_stage_buffer(self.h, scheme, stage - 1, _ptr(u), ctypes.byref(out)),
+                   "hd_stage_buffer")
+        if out.value == u.data_ptr():
+            return u
+        off = out.value - self.ws.data_ptr()
+        n = 5 * self.npts
+        return self.ws[off: off + 8 * n].view(torch.float64)
+
     # ---- peer halo over NVLink (z slabs) ----------------------------------
     def ipc_handle(self) -> tuple:
         """(64-byte IPC handle, offset) of this plan's workspace for a z neighbour."""
