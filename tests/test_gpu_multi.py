@@ -88,6 +88,51 @@ def test_z_slab_nccl_halo_equals_single_gpu(tmp_path, traj32_golden):
         assert r["sha"] == traj32_golden["final_sha256"], r["dims"]
 
 
+TF_SCRIPT = r'''
+import json, os, sys
+sys.path.insert(0, os.environ["HD_ROOT"])
+import torch, torch.distributed as dist
+import paper_2211_16718_b200 as hd
+rank = int(os.environ["RANK"])
+torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+spec = hd.GridSpec((32, 32, 32))
+ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+res = hd.parallel_advance(ic, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", cfl=0.4, t_final=0.2),
+                          mode="exact")
+if rank == 0:
+    with open(os.path.join(os.environ["HD_OUT"], "tf.json"), "w") as fh:
+        json.dump({"t": res.t, "steps": res.reports[0].steps,
+                   "data": res.fields.interior().cpu().numpy().tobytes().hex()[:4096]}, fh)
+dist.destroy_process_group()
+'''
+
+
+def test_t_final_march_on_two_gpus(tmp_path):
+    """The host-synchronised march (t_final clipping, timeint.py:222-227) through the
+    peer-store halo lands on t_final exactly and equals the single-GPU march."""
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import paper_2211_16718_b200 as hd
+
+    path = tmp_path / "tf.py"
+    path.write_text(TF_SCRIPT)
+    env = dict(os.environ, HD_ROOT=ROOT, HD_OUT=str(tmp_path))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29545",
+                          str(path)], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    with open(tmp_path / "tf.json") as fh:
+        multi = json.load(fh)
+    spec = hd.GridSpec((32, 32, 32))
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+    res = hd.advance(ic, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", cfl=0.4, t_final=0.2),
+                     mode="exact")
+    assert res.t == multi["t"] == 0.2 and res.steps == multi["steps"]
+    assert res.fields.interior().cpu().numpy().tobytes().hex()[:4096] == multi["data"]
+
+
 def test_cli_scale_relaunches_one_process_per_gpu():
     """``scale`` outside torchrun relaunches itself with one rank per GPU and
     prints the reference's table (decomp.py:464-476) for each rank count."""
