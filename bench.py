@@ -53,7 +53,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--grid", "--n", dest="n", type=int, default=512,
+                    help="cube size (use --grid under torchrun: --n collides with its options)")
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
