@@ -335,8 +335,7 @@ class DistHalo:
 
         def reducer(red):
             if self.split:
-                dist.all_reduce(red[0:3], op=dist.ReduceOp.MAX, group=halo.group)
-                dist.all_reduce(red[3:9], op=dist.ReduceOp.SUM, group=halo.group)
+                _combine_reductions(red, halo.group)
 
         nblocks = self.layout.dims[0] * self.layout.dims[1] * self.layout.dims[2]
         march = _DeviceMarch(plan, fields, gas, tparams, t0, stepper=stepper, reducer=reducer,
@@ -391,8 +390,7 @@ class DistHalo:
                     counter[0] = v
 
             def reducer(red):
-                dist.all_reduce(red[0:3], op=dist.ReduceOp.MAX, group=self.group)
-                dist.all_reduce(red[3:9], op=dist.ReduceOp.SUM, group=self.group)
+                _combine_reductions(red, self.group)
 
             march = _DeviceMarch(plan, local, gas, tparams, t0, stepper=stepper, reducer=reducer,
                                  global_points=spec.interior_points * self.layout.dims[2],
@@ -408,6 +406,20 @@ class DistHalo:
         _check_protocol(not timed_out, "a z neighbour never signalled (peer halo timed out)")
         res.fields = FieldSet(spec, Layout.COMPONENT_CONTIGUOUS, state.clone())
         return res
+
+
+def _combine_reductions(red: torch.Tensor, group) -> None:
+    """The per-step reduction over ranks in one collective: all-gather the
+    HD_RED_* vectors, then MAX the signals (exact) and SUM the totals in rank
+    order (deterministic) on the device."""
+    world = dist.get_world_size(group)
+    allv = torch.empty((world, red.numel()), dtype=red.dtype, device=red.device)
+    dist.all_gather_into_tensor(allv, red.contiguous(), group=group)
+    red[0:3] = allv[:, 0:3].amax(dim=0)
+    acc = allv[0, 3:].clone()
+    for r in range(1, world):
+        acc += allv[r, 3:]
+    red[3:] = acc
 
 
 def _combine_error_key(key: int, group) -> int:
