@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("HD_LIB") or os.path.join(HERE, "libhd.so")
 CSRC = os.path.join(HERE, "csrc")
 
 HD_OK = 0
+HD_E_ARG, HD_E_CUDA, HD_E_WORKSPACE, HD_E_UNSUPPORTED = -1, -2, -3, -4
 HD_MODE_FAST = 0
 HD_MODE_EXACT = 1
 HD_SCHEME_RK3 = 3
