@@ -71,7 +71,7 @@ extern "C" {
 #define HD_BUF_CTX 6   /* step context: t, dt, ... */
 #define HD_BUF_ERR 7   /* error key (uint64) */
 #define HD_BUF_STATE 8 /* 5 fields: march state of a peer-attached plan (hd_peer_attach) */
-#define HD_BUF_SYNC 9  /* 8 uint64: peer flags (state from lo/hi, vflux from lo/hi), timeout word */
+#define HD_BUF_SYNC 9  /* 16 uint64: peer flags [axis][state|vflux][from lo|hi], timeout word */
 #define HD_NBUF 10
 
 /* results of hd_reduce_state (doubles at HD_BUF_RED result slot) */
@@ -238,12 +238,15 @@ int hd_ipc_handle(const void* ptr, void* handle64, int64_t* offset);
 int hd_ipc_open(const void* handle64, int64_t offset, void** ptr);
 /* Unmap (pass the pointer hd_ipc_open returned and its offset). */
 int hd_ipc_close(void* ptr, int64_t offset);
-/* lo_ws / hi_ws: the neighbours' workspaces as mapped here (may be equal: two
- * ranks); NULL, NULL detaches.  Zeroes this plan's flags (call before any peer
- * can signal, then barrier). */
+/* lo_ws[d] / hi_ws[d]: the neighbours' workspaces along axis d as mapped here
+ * (may be equal: two blocks along d), NULL for an axis that is not split (it
+ * must then be periodic); all NULL detaches.  Zeroes this plan's flags (call
+ * before any peer can signal, then barrier). */
+int hd_peer_attach3(hd_plan* plan, void* const* lo_ws, void* const* hi_ws, void* stream);
+/* z slabs only: hd_peer_attach3 with lo/hi along z. */
 int hd_peer_attach(hd_plan* plan, void* lo_ws, void* hi_ws, void* stream);
 int hd_peer_signal(hd_plan* plan, int which, int64_t value, void* stream);
-/* Stream waits until both neighbours signalled >= value (spins at most
+/* Stream waits until every neighbour signalled >= value (spins at most
  * ~30 s, then sets the timeout word of HD_BUF_SYNC and lets the stream go). */
 int hd_peer_wait(hd_plan* plan, int which, int64_t value, void* stream);
 /* 1 if a wait timed out since the attach. */

@@ -40,7 +40,7 @@ EXPORTS = (
     "hd_hyper_sweep", "hd_hyperbolic_rhs", "hd_parabolic_rhs", "hd_central_diff4", "hd_rhs",
     "hd_step", "hd_stage_part", "hd_reduce_state", "hd_set_dt", "hd_commit_time",
     "hd_error_read", "hd_error_clear", "hd_fp64_probe", "hd_bench_weights", "hd_launch_counter", "hd_timer_enable",
-    "hd_timer_read", "hd_ipc_handle", "hd_ipc_open", "hd_ipc_close", "hd_peer_attach", "hd_peer_signal",
+    "hd_timer_read", "hd_ipc_handle", "hd_ipc_open", "hd_ipc_close", "hd_peer_attach", "hd_peer_attach3", "hd_peer_signal",
     "hd_peer_wait", "hd_peer_timed_out", "hd_stage_buffer",
 )
 # hd_timer_read kinds (HD_TK_*)
@@ -123,6 +123,7 @@ def load(require_cuda: bool = False):
             "hd_ipc_open": ([P, i64, ctypes.POINTER(ctypes.c_void_p)], i32),
             "hd_ipc_close": ([P, i64], i32),
             "hd_peer_attach": ([P, P, P, P], i32),
+            "hd_peer_attach3": ([P, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p), P], i32),
             "hd_peer_signal": ([P, i32, i64, P], i32),
             "hd_peer_wait": ([P, i32, i64, P], i32),
             "hd_peer_timed_out": ([P, ctypes.POINTER(ctypes.c_int), P], i32),

@@ -49,7 +49,7 @@ void layout(const hd_geom* g, int64_t off[HD_NBUF], int64_t* total) {
   const int64_t f = npts_of(g) * 8;
   int64_t o = 0;
   const int64_t sizes[HD_NBUF] = {10 * f, 5 * f, 5 * f, 4 * f, 9 * f, RED_BYTES, 8 * HD_CTX_N, 64,
-                                  5 * f, 64};
+                                  5 * f, 128};
   for (int b = 0; b < HD_NBUF; ++b) {
     off[b] = o;
     o = align_up(o + sizes[b]);
@@ -343,7 +343,7 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   if (!rc && (parts & HD_PART_UPDATE)) {
     if (!dt_dev) return HD_E_ARG;
     // peer mode: the final stage's images land in the neighbours' HD_BUF_STATE
-    if (p->geo.zpeer && u != buf(p, HD_BUF_STATE)) return HD_E_ARG;
+    if (p->geo.peer_any && u != buf(p, HD_BUF_STATE)) return HD_E_ARG;
     if (exact)
       rc = timed(p, HD_TK_DIVERGENCE, s, [&] {
         return launch_divergence(p, visc ? 7 : 0, inc, nullptr, 1, scheme, stage, u, dt_dev, s);

@@ -55,10 +55,18 @@ __device__ __forceinline__ void store_with_images(double* f, const Geo& G, int i
       for (int a = 0; a < nx; ++a) f[G.idx(i + ox[a], j + oy[b], k + oz[c])] = v;
 }
 
-// axes whose face images kernels write: locally periodic axes, and z when the
-// images go to the z neighbours' ghost planes (peer stores, Geo::zpeer)
+// axes whose face images kernels write: locally periodic axes, and split axes
+// whose images go to the neighbours' ghost planes (peer stores, Geo::peer)
 __device__ __forceinline__ int periodic_mask(const Geo& G) {
-  return (G.periodic[0] ? 1 : 0) | (G.periodic[1] ? 2 : 0) | ((G.periodic[2] || G.zpeer) ? 4 : 0);
+  return ((G.periodic[0] || G.peer[0]) ? 1 : 0) | ((G.periodic[1] || G.peer[1]) ? 2 : 0) |
+         ((G.periodic[2] || G.peer[2]) ? 4 : 0);
+}
+
+// does the point (i,j,k) have a face image that lands in a neighbour's buffer?
+__device__ __forceinline__ bool touches_peer(const Geo& G, int i, int j, int k) {
+  const int g = G.g;
+  return (G.peer[0] && (i < g || i >= G.n[0] - g)) || (G.peer[1] && (j < g || j >= G.n[1] - g)) ||
+         (G.peer[2] && (k < g || k >= G.n[2] - g));
 }
 
 
@@ -69,17 +77,18 @@ __device__ __forceinline__ void store_face_images(double* f, const Geo& G, int i
                                                   int mask, double v) {
   f[G.idx(i, j, k)] = v;
   const int g = G.g;
+  // peer axes: the image lands in the neighbour's buffer (peer_lo/hi deltas)
   if (mask & 1) {
-    if (i < g) f[G.idx(i + G.n[0], j, k)] = v;
-    if (i >= G.n[0] - g) f[G.idx(i - G.n[0], j, k)] = v;
+    if (i < g) f[G.idx(i + G.n[0], j, k) + G.peer_lo[0]] = v;
+    if (i >= G.n[0] - g) f[G.idx(i - G.n[0], j, k) + G.peer_hi[0]] = v;
   }
   if (mask & 2) {
-    if (j < g) f[G.idx(i, j + G.n[1], k)] = v;
-    if (j >= G.n[1] - g) f[G.idx(i, j - G.n[1], k)] = v;
+    if (j < g) f[G.idx(i, j + G.n[1], k) + G.peer_lo[1]] = v;
+    if (j >= G.n[1] - g) f[G.idx(i, j - G.n[1], k) + G.peer_hi[1]] = v;
   }
-  if (mask & 4) {  // peer mode: into the z neighbours' ghost planes
-    if (k < g) f[G.idx(i, j, k + G.n[2]) + G.zpeer_lo] = v;
-    if (k >= G.n[2] - g) f[G.idx(i, j, k - G.n[2]) + G.zpeer_hi] = v;
+  if (mask & 4) {
+    if (k < g) f[G.idx(i, j, k + G.n[2]) + G.peer_lo[2]] = v;
+    if (k >= G.n[2] - g) f[G.idx(i, j, k - G.n[2]) + G.peer_hi[2]] = v;
   }
 }
 
@@ -203,16 +212,16 @@ __device__ __forceinline__ int face_image_deltas(const Geo& G, int i, int j, int
   const int g = G.g;
   // both images of an axis when the block is thinner than 2g along it
   if (mask & 1) {
-    if (i < g) dl[nd++] = G.n[0];
-    if (i >= G.n[0] - g) dl[nd++] = -(int64_t)G.n[0];
+    if (i < g) dl[nd++] = G.n[0] + G.peer_lo[0];
+    if (i >= G.n[0] - g) dl[nd++] = -(int64_t)G.n[0] + G.peer_hi[0];
   }
   if (mask & 2) {
-    if (j < g) dl[nd++] = (int64_t)G.n[1] * G.sy;
-    if (j >= G.n[1] - g) dl[nd++] = -(int64_t)G.n[1] * G.sy;
+    if (j < g) dl[nd++] = (int64_t)G.n[1] * G.sy + G.peer_lo[1];
+    if (j >= G.n[1] - g) dl[nd++] = -(int64_t)G.n[1] * G.sy + G.peer_hi[1];
   }
   if (mask & 4) {
-    if (k < g) dl[nd++] = (int64_t)G.n[2] * G.sz + G.zpeer_lo;
-    if (k >= G.n[2] - g) dl[nd++] = -(int64_t)G.n[2] * G.sz + G.zpeer_hi;
+    if (k < g) dl[nd++] = (int64_t)G.n[2] * G.sz + G.peer_lo[2];
+    if (k >= G.n[2] - g) dl[nd++] = -(int64_t)G.n[2] * G.sz + G.peer_hi[2];
   }
   return nd;
 }

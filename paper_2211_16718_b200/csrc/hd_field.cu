@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict_
 #pragma unroll
   for (int f = 0; f < VF_N; ++f)
     store_face_images(vf + (int64_t)f * np, G, i, j, k, pm & vf_axes(f), val[f]);
-  if (G.zpeer && (k < G.g || k >= G.n[2] - G.g)) __threadfence_system();
+  if (G.peer_any && touches_peer(G, i, j, k)) __threadfence_system();
 }
 
 // gradflux with z marching (blocks of 32 x 8 columns): the z stencil comes from
@@ -356,21 +356,23 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, HD_GZ_MINB) gradflux_zm_kernel(
       F[0] = v;
       const int axes = vf_axes(f);
       if (axes & 1) {
-        if (xl) F[G.n[0]] = v;
-        if (xh) F[-G.n[0]] = v;
+        if (xl) F[G.n[0] + G.peer_lo[0]] = v;
+        if (xh) F[-G.n[0] + G.peer_hi[0]] = v;
       }
       if (axes & 2) {
-        if (yl) F[dy] = v;
-        if (yh) F[-dy] = v;
+        if (yl) F[dy + G.peer_lo[1]] = v;
+        if (yh) F[-dy + G.peer_hi[1]] = v;
       }
       if (axes & 4) {
-        if (zl) F[dz + G.zpeer_lo] = v;
-        if (zh) F[-dz + G.zpeer_hi] = v;
+        if (zl) F[dz + G.peer_lo[2]] = v;
+        if (zh) F[-dz + G.peer_hi[2]] = v;
       }
     }
   }
-  // peer stores performed before the kernel ends (only segments holding boundary planes)
-  if (G.zpeer && (k0 < G.g || k1 > G.n[2] - G.g)) __threadfence_system();
+  // peer stores performed before the kernel ends (threads that made any)
+  if (G.peer_any && ((G.peer[2] && (k0 < G.g || k1 > G.n[2] - G.g)) ||
+                     touches_peer(G, i, j, G.g)))
+    __threadfence_system();
 }
 
 
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(128) divergence_kernel(const double* __restric
   add_viscous_divergence<EXACT>(vf, G, q, dmask, kv);
   if (update) {
     rk_store<EXACT>(r, G, i, j, k, kv);
-    if (G.zpeer && (k < G.g || k >= G.n[2] - G.g)) __threadfence_system();
+    if (G.peer_any && touches_peer(G, i, j, k)) __threadfence_system();
   } else {
 #pragma unroll
     for (int v = 0; v < NV; ++v) inc_out[q + v * np] = kv[v];

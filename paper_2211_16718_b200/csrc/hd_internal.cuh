@@ -67,10 +67,12 @@ struct Geo {
   int64_t sy, sz;  // strides of y and z in points (sx = 1)
   double h[3];  // spacing
   int periodic[3];
-  // peer z images (hd_peer_attach): element deltas from a local buffer to the
-  // same buffer of the lower / upper z neighbour, mapped into this process
-  int zpeer;
-  int64_t zpeer_lo, zpeer_hi;
+  // peer images (hd_peer_attach3): per axis, element deltas from a local
+  // buffer to the same buffer of the lower / upper neighbour, mapped into this
+  // process; peer[d] = 1 when axis d's face images go to the neighbours
+  int peer[3];
+  int64_t peer_lo[3], peer_hi[3];
+  int peer_any;
 
   __host__ __device__ int64_t idx(int i, int j, int k) const {  // interior coords, may be in ghosts
     return ((int64_t)(k + g) * gn[1] + (j + g)) * gn[0] + (i + g);
@@ -108,8 +110,8 @@ struct hd_plan {
   int device;
   int sm_count;
   void* timer;  // per-kernel event timer (hd_timer_enable), owned
-  char* peer_lo;  // z neighbours' workspaces mapped here (hd_peer_attach), not owned
-  char* peer_hi;
+  char* peer_lo[3];  // neighbours' workspaces mapped here (hd_peer_attach3), not owned
+  char* peer_hi[3];
 };
 
 namespace hd {

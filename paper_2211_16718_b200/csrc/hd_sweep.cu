@@ -605,7 +605,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
     }
   }
   // peer stores (this line segment held boundary planes) performed before the kernel ends
-  if (ROLE == ROLE_UPDATE && DIM == 2 && G.zpeer && (c0 < G.g || c1 > nd - G.g))
+  if (ROLE == ROLE_UPDATE && DIM == 2 && G.peer_any &&
+      ((G.peer[2] && (c0 < G.g || c1 > nd - G.g)) || touches_peer(G, li, lj, G.g)))
     __threadfence_system();
 }
 

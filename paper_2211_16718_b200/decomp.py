@@ -344,22 +344,26 @@ class DistHalo:
         return march.run(observer, dt_provider)
 
     def peer_enabled(self, fields: FieldSet) -> bool:
-        """z-slab blocks on CUDA: the halo goes over NVLink peer stores (hd_peer_*)
+        """Blocks on CUDA: the halo goes over NVLink peer stores (hd_peer_*)
         instead of NCCL, unless HD_PEER=0."""
-        return (self.split == (2,) and fields.data.is_cuda
+        return (bool(self.split) and fields.data.is_cuda
                 and os.environ.get("HD_PEER", "1") not in ("0", ""))
 
     def _advance_peer(self, plan, fields: FieldSet, gas: GasModel, tparams, t0, observer,
                       dt_provider):
-        """The z-slab march with the halo fused into the producing kernels: the z
-        sweep's RK update and the flux kernel store their boundary planes into
-        the z neighbours' ghost planes over NVLink; per RK stage v
+        """The block march with the halo fused into the producing kernels: the z
+        sweep's RK update and the flux kernel store their boundary layers into
+        the neighbours' ghost layers over NVLink along every split axis; per RK
+        stage v (fast mode, z split only)
 
             LOCAL; wait(state >= v-1); HALO; signal(vflux, v); MID;
             wait(vflux >= v); UPDATE; signal(state, v)
 
-        (include/hd.h, hd_peer.cu).  The march state lives in the plan's
-        HD_BUF_STATE so the peers' images land at the same offsets."""
+        with the state wait moved before LOCAL when x is split (the x sweep reads
+        x ghosts) and the flux wait before MID when x or y is split (the y sweep
+        differentiates the x and y flux groups) (include/hd.h, hd_peer.cu).  The
+        march state lives in the plan's HD_BUF_STATE so the peers' images land at
+        the same offsets."""
         from .timeint import _SCHEME_CODE, _DeviceMarch
 
         spec = fields.spec
@@ -370,20 +374,30 @@ class DistHalo:
         state.copy_(fields.data)
         local = FieldSet(spec, Layout.COMPONENT_CONTIGUOUS, state)
         try:
-            self.exchange_async(state, NVARS, spec, axes=(2,)).wait()  # initial z ghosts
+            self._sync(state, NVARS, spec)  # initial ghosts (wrap + NCCL faces, once)
             counter = [0]
 
+            # LOCAL reads x ghosts (exact mode: also y); MID reads the x/y flux groups
+            exact = plan.mode == "exact"
+            state_before_local = 0 in self.split or (exact and 1 in self.split)
+            vflux_before_mid = not exact and (0 in self.split or 1 in self.split)
+
             def stepper(u, dt_dev, tag):
-                plan.fill_ghosts(u, NVARS)  # x/y wrap; z ghosts arrive as peer stores
+                plan.fill_ghosts(u, NVARS)  # periodic axes wrap; split axes arrive as peer stores
                 for s in range(nst):
                     v = counter[0] + 1
+                    if state_before_local:
+                        plan.peer_wait(_lib.HD_PEER_STATE, v - 1)
                     plan.stage_part(scheme, s, _lib.HD_PART_LOCAL, u, dt_dev, tag)
-                    plan.peer_wait(_lib.HD_PEER_STATE, v - 1)
+                    if not state_before_local:
+                        plan.peer_wait(_lib.HD_PEER_STATE, v - 1)
                     plan.stage_part(scheme, s, _lib.HD_PART_HALO, u, dt_dev, tag)
                     if visc:
                         plan.peer_signal(_lib.HD_PEER_VFLUX, v)
+                        if vflux_before_mid:
+                            plan.peer_wait(_lib.HD_PEER_VFLUX, v)
                     plan.stage_part(scheme, s, _lib.HD_PART_MID, u, dt_dev, tag)
-                    if visc:
+                    if visc and not vflux_before_mid:
                         plan.peer_wait(_lib.HD_PEER_VFLUX, v)
                     plan.stage_part(scheme, s, _lib.HD_PART_UPDATE, u, dt_dev, tag)
                     plan.peer_signal(_lib.HD_PEER_STATE, v)
@@ -392,8 +406,9 @@ class DistHalo:
             def reducer(red):
                 _combine_reductions(red, self.group)
 
+            nblocks = self.layout.dims[0] * self.layout.dims[1] * self.layout.dims[2]
             march = _DeviceMarch(plan, local, gas, tparams, t0, stepper=stepper, reducer=reducer,
-                                 global_points=spec.interior_points * self.layout.dims[2],
+                                 global_points=spec.interior_points * nblocks,
                                  copy=False,
                                  error_combine=lambda key: _combine_error_key(key, self.group))
             res = march.run(observer, dt_provider)
@@ -402,7 +417,7 @@ class DistHalo:
             dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
             timed_out = bool(flag.item())
         finally:
-            plan.peer_attach(None, None)  # the mapping stays cached (_PeerLink)
+            plan.peer_attach([None] * 3, [None] * 3)  # the mapping stays cached (_PeerLink)
         _check_protocol(not timed_out, "a z neighbour never signalled (peer halo timed out)")
         res.fields = FieldSet(spec, Layout.COMPONENT_CONTIGUOUS, state.clone())
         return res
@@ -477,7 +492,7 @@ class _PeerLink:
             dist.all_gather_object(allh, (handle, off), group=halo.group)
             self.release()
             ok = 1
-            for r in {halo.lo[2], halo.hi[2]}:
+            for r in {n for d in halo.split for n in (halo.lo[d], halo.hi[d])}:
                 h, o = allh[r]
                 ptr = ctypes.c_void_p()
                 if self.L.hd_ipc_open(ctypes.create_string_buffer(h, 64), o, ctypes.byref(ptr)) != 0:
@@ -490,7 +505,9 @@ class _PeerLink:
                 self.release()
                 return False  # every rank falls back to the NCCL halo together
             self.digests = digests
-        plan.peer_attach(self.opened[halo.lo[2]][0], self.opened[halo.hi[2]][0])  # zeroes flags
+        lo = [self.opened[halo.lo[d]][0] if d in halo.split else None for d in range(3)]
+        hi = [self.opened[halo.hi[d]][0] if d in halo.split else None for d in range(3)]
+        plan.peer_attach(lo, hi)  # zeroes the flags
         torch.cuda.synchronize()
         dist.barrier(group=halo.group)  # every rank's flags are zero before anyone signals
         return True

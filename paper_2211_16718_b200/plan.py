@@ -205,9 +205,11 @@ class Plan:
                                         ctypes.byref(off)), "hd_ipc_handle")
         return bytes(h), int(off.value)
 
-    def peer_attach(self, lo_ptr: int | None, hi_ptr: int | None) -> None:
-        _lib.check(self.L.hd_peer_attach(self.h, ctypes.c_void_p(lo_ptr), ctypes.c_void_p(hi_ptr),
-                                         _stream_ptr()), "hd_peer_attach")
+    def peer_attach(self, lo, hi) -> None:
+        """Neighbours' workspace pointers per axis (None for an unsplit axis)."""
+        lo3 = (ctypes.c_void_p * 3)(*[ctypes.c_void_p(p) for p in lo])
+        hi3 = (ctypes.c_void_p * 3)(*[ctypes.c_void_p(p) for p in hi])
+        _lib.check(self.L.hd_peer_attach3(self.h, lo3, hi3, _stream_ptr()), "hd_peer_attach3")
 
     def peer_signal(self, which: int, value: int) -> None:
         _lib.check(self.L.hd_peer_signal(self.h, which, value, _stream_ptr()), "hd_peer_signal")
