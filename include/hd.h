@@ -217,18 +217,20 @@ int hd_fp64_probe(double* out, int blocks, int threads, int iters, void* stream)
  * what a decomposed driver exchanges between the stage parts. */
 int hd_stage_buffer(hd_plan* plan, int scheme, int stage, double* u, void** out);
 
-/* ---- peer halo over NVLink (z slabs, one process per GPU) -------------------
- * Replaces the NCCL face exchange of a z-slab decomposition (decomp.py:183-241
- * RankHalo) for a plan whose z axis is not periodic: with the workspaces of the
- * lower and upper z neighbours mapped into this process (hd_ipc_open of their
- * hd_ipc_handle), every kernel that writes a stage state or a z-differentiated
- * viscous flux stores the values of its g boundary planes straight into the
- * neighbour's ghost planes (peer stores over NVLink; the same index deltas as
- * the periodic images).  Requires the march state to live in HD_BUF_STATE.
- * Protocol per RK stage with a counter v (1, 2, ...):
+/* ---- peer halo over NVLink (block decompositions, one process per GPU) ------
+ * Replaces the face exchange of the reference's RankHalo (decomp.py:183-241)
+ * for a plan whose split axes are not periodic: with the workspaces of the
+ * lower and upper neighbours along every split axis mapped into this process
+ * (hd_ipc_open of their hd_ipc_handle), every kernel that writes a stage state
+ * or a viscous flux field stores the values of its g boundary layers straight
+ * into the neighbours' ghost layers (peer stores over NVLink; the same index
+ * deltas as the periodic images).  Requires the march state to live in
+ * HD_BUF_STATE.  Protocol per RK stage with a counter v (1, 2, ...), z split:
  *   LOCAL; hd_peer_wait(STATE, v-1); HALO; hd_peer_signal(VFLUX, v); MID;
  *   hd_peer_wait(VFLUX, v); UPDATE; hd_peer_signal(STATE, v)
- * (the two halves of HD_BUF_STAGE make every write-after-read safe). */
+ * -- the STATE wait before LOCAL when x is split, the VFLUX wait before MID
+ * when x or y is split (the two halves of HD_BUF_STAGE make every
+ * write-after-read safe). */
 #define HD_PEER_STATE 0
 #define HD_PEER_VFLUX 1
 /* 64-byte IPC handle + byte offset of `ptr` inside its allocation. */
