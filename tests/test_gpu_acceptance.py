@@ -116,3 +116,61 @@ def test_torch_ic_is_reproducible(hd):
     a = hd.make_initial_condition(spec, hd.HitParams(), backend="torch").data
     b = hd.make_initial_condition(spec, hd.HitParams(), backend="torch").data
     assert torch.equal(a, b)
+
+
+GAMMA_HIT = 1.4
+
+
+def _vel(fields):
+    it = fields.interior()
+    return it[1] / it[0], it[2] / it[0], it[3] / it[0]
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_inviscid_hundred_step_conservation(hd, mode):
+    """pkg/tests/test_acceptance.py:315-341 as written: 64^3, mu = 0, the default
+    TimeParams scheme (RK3), CFL 0.4, 100 steps; drifts < 1e-11."""
+    params = hd.HitParams()
+    spec = hd.GridSpec((64, 64, 64))
+    fields = hd.make_initial_condition(spec, params, GAMMA_HIT, backend="numpy")
+    mass0, mom0, energy0 = hd.conserved_totals(fields)
+    res = hd.advance(fields, hd.GasModel(mu=0.0), hd.TimeParams(cfl=0.4, max_steps=100), mode=mode)
+    mass1, mom1, energy1 = hd.conserved_totals(res.fields)
+    mom_scale = params.rho0 * params.u0 * (2 * math.pi) ** 3
+    assert abs(mass1 - mass0) / abs(mass0) < 1e-11
+    assert abs(energy1 - energy0) / abs(energy0) < 1e-11
+    assert max(abs(a - b) / max(abs(b), mom_scale) for a, b in zip(mom1, mom0)) < 1e-11
+
+
+def test_decaying_turbulence_cascades_energy_to_small_scales(hd):
+    """pkg/tests/test_acceptance.py:352-373: three eddy turnovers (t = 10) of
+    viscous decay at 64^3 -- the high-wavenumber band fills, total KE falls."""
+    params = hd.HitParams()
+    spec = hd.GridSpec((64, 64, 64))
+    fields = hd.make_initial_condition(spec, params, GAMMA_HIT, backend="numpy")
+    before = hd.compute_spectrum(*_vel(fields))
+    gas = hd.GasModel(mu=hd.viscosity_from_re_lambda(params))
+    res = hd.advance(fields, gas, hd.TimeParams(cfl=0.4, t_final=10.0))
+    after = hd.compute_spectrum(*_vel(res.fields))
+    assert res.t == 10.0
+    assert float(np.sum(after.energy[16:])) > float(np.sum(before.energy[16:]))
+    assert after.total() < before.total()
+
+
+def test_fast_mode_ke_curve_tracks_exact(hd):
+    """The north-star tolerance over a long march: 64^3 HIT, RK4, 100 steps; the
+    fast arithmetic's kinetic-energy curve stays within 1e-11 of the bitwise-
+    reference curve at every step and the final state within 1e-10 relative L2."""
+    spec = hd.GridSpec((64, 64, 64))
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+    gas = hd.GasModel(mu=0.006)
+    tp = hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=100)
+    ex = hd.advance(ic, gas, tp, mode="exact")
+    fa = hd.advance(ic, gas, tp, mode="fast")
+    ke_ex = np.array([r.kinetic_energy for r in ex.records])
+    ke_fa = np.array([r.kinetic_energy for r in fa.records])
+    assert np.max(np.abs(ke_fa - ke_ex) / ke_ex) < 1e-11
+    a = ex.fields.interior().reshape(5, -1)
+    b = fa.fields.interior().reshape(5, -1)
+    rel = ((b - a).norm(dim=1) / a.norm(dim=1)).cpu().numpy()
+    assert np.all(rel <= 1e-10), rel
