@@ -217,6 +217,23 @@ int hd_fp64_probe(double* out, int blocks, int threads, int iters, void* stream)
  * what a decomposed driver exchanges between the stage parts. */
 int hd_stage_buffer(hd_plan* plan, int scheme, int stage, double* u, void** out);
 
+/* ---- single-operation entry points (the names of SURVEY.md 8b) --------------- */
+/* classical RK4 step (timeint.py:181-193) = hd_step(plan, HD_SCHEME_RK4, u, dt, 0, 0). */
+int hd_rk4_step(hd_plan* plan, double* u, const double* dt_dev, void* stream);
+/* CFL signal of the interior (timeint.py:122-131) into out_dev[0]: mode 0 = max
+ * over points and directions of (|v_d| + a)/h_d, 1 = max of the sum over d. */
+int hd_max_signal(hd_plan* plan, const double* u, double* out_dev, int mode, void* stream);
+/* Volume-weighted mass, momentum (3), energy (timeint.py:100-107) into out5_dev. */
+int hd_totals(hd_plan* plan, const double* u, double* out5_dev, void* stream);
+/* The latched error as flags: bit0 nonpositive density, bit1 nonpositive
+ * pressure, bit2 bad CFL signal; *where = flat point index (or -1). */
+int hd_error_flags(hd_plan* plan, int* flags, int64_t* where, void* stream);
+/* Ghost layers of `fields` (nfields x total points): periodic axes wrap
+ * (grid.py:236-251); on a peer-attached plan the boundary layers along the
+ * split axes are stored into the neighbours' ghost layers (`fields` must be a
+ * buffer of the plan workspace; order it with hd_peer_signal / hd_peer_wait). */
+int hd_halo_exchange(hd_plan* plan, double* fields, int nfields, void* stream);
+
 /* ---- peer halo over NVLink (block decompositions, one process per GPU) ------
  * Replaces the face exchange of the reference's RankHalo (decomp.py:183-241)
  * for a plan whose split axes are not periodic: with the workspaces of the

@@ -13,7 +13,7 @@ for spec in "$@"; do
   done
   out=../../build/variants/$name
   mkdir -p $out
-  for f in hd_sweep hd_field hd_api hd_bench hd_peer; do
+  for f in hd_sweep hd_field hd_api hd_bench hd_peer hd_compat; do
     /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $defs -Xptxas -v -c $f.cu -o $out/$f.o 2> $out/$f.ptxas.log &
   done
   wait
