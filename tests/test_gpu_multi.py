@@ -248,3 +248,76 @@ def test_512_z_slabs_equal_single_gpu_bitwise(tmp_path):
     hd.release_plans()
     assert hashlib.sha256(body.tobytes()).hexdigest() == multi["sha"]
     assert res.t == multi["t"]
+
+
+HX_SCRIPT = r'''
+import json, os, sys, ctypes
+sys.path.insert(0, os.environ["HD_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+import paper_2211_16718_b200 as hd
+from paper_2211_16718_b200 import _lib
+from paper_2211_16718_b200.decomp import _PeerLink
+rank = int(os.environ["RANK"]); world = int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+dims = tuple(json.loads(os.environ["HD_DIMS"]))
+spec = hd.GridSpec((16, 16, 16))
+lay = hd.decompose(spec, dims)[rank]
+halo = hd.DistHalo(lay)
+plan = hd.get_plan(lay.spec, hd.GasModel(), periodic=halo.periodic)
+assert _PeerLink.get(halo).attach(plan)
+state = plan.fields(_lib.HD_BUF_STATE, 5)
+# global field with known values: f(var, z, y, x) = var*1e6 + zg*1e4 + yg*1e2 + xg
+g = spec.ghost_width
+ln = lay.local_n
+v = state.view((5,) + lay.spec.shape)
+v.zero_()
+z = torch.arange(ln[2], device="cuda")[:, None, None] + lay.offset[2]
+y = torch.arange(ln[1], device="cuda")[None, :, None] + lay.offset[1]
+x = torch.arange(ln[0], device="cuda")[None, None, :] + lay.offset[0]
+for c in range(5):
+    v[c, g:-g, g:-g, g:-g] = (c * 1e6 + z * 1e4 + y * 1e2 + x).double()
+torch.cuda.synchronize(); dist.barrier()
+L = _lib.load()
+s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+assert L.hd_halo_exchange(plan.h, ctypes.c_void_p(state.data_ptr()), 5, s) == 0
+torch.cuda.synchronize(); dist.barrier()
+# every face ghost (interior extent of the other axes) holds the periodic neighbour's value
+ok = True
+for d in range(3):
+    for side in (0, 1):
+        ax = 2 - d
+        idx = list(range(0, g)) if side == 0 else list(range(ln[d] + g, ln[d] + 2 * g))
+        got = v[0].index_select(ax, torch.tensor(idx, device="cuda"))
+        got = got[tuple(slice(g, g + ln[2 - a]) if a != ax else slice(None) for a in range(3))]
+        coord = torch.tensor([(lay.offset[d] + i - g) % spec.n[d] for i in idx], device="cuda").double()
+        zz = (torch.arange(ln[2], device="cuda") + lay.offset[2]).double()
+        yy = (torch.arange(ln[1], device="cuda") + lay.offset[1]).double()
+        xx = (torch.arange(ln[0], device="cuda") + lay.offset[0]).double()
+        comps = [zz, yy, xx]
+        comps[ax] = coord
+        want = comps[0][:, None, None] * 1e4 + comps[1][None, :, None] * 1e2 + comps[2][None, None, :]
+        ok = ok and bool(torch.equal(got, want))
+plan.peer_attach([None] * 3, [None] * 3)
+with open(os.path.join(os.environ["HD_OUT"], f"hx{rank}.json"), "w") as fh:
+    json.dump({"ok": ok}, fh)
+dist.destroy_process_group()
+'''
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 2), (2, 1, 1), (1, 2, 1)])
+def test_halo_exchange_entry_point_peer(tmp_path, dims):
+    """hd_halo_exchange on a peer-attached plan: every face ghost layer holds the
+    neighbour's boundary layer (split axes) or the local wrap (periodic axes)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    path = tmp_path / "hx.py"
+    path.write_text(HX_SCRIPT)
+    env = dict(os.environ, HD_ROOT=ROOT, HD_OUT=str(tmp_path), HD_DIMS=json.dumps(dims))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29547",
+                          str(path)], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    for r in range(2):
+        with open(tmp_path / f"hx{r}.json") as fh:
+            assert json.load(fh)["ok"], r
