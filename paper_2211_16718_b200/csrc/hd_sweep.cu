@@ -910,9 +910,6 @@ int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, co
   SweepArgs a = make_args(p, 2, u_stage, inc, 1, 0, tag, nseg);
   a.vflux = vflux;
   a.prim = prim;
-  // cost-attribution switches for profiling only (results are wrong with them set)
-  if (getenv_flag("HD_PROFILE_NO_DZ")) a.vflux = nullptr;
-  if (getenv_flag("HD_PROFILE_NO_PRIMS")) a.prim = nullptr;
   a.rk = make_rk(p, scheme, stage, u, dt_dev);
   if (p->mode == HD_MODE_EXACT) return HD_E_UNSUPPORTED;  // exact mode runs the unfused stage
   return launch_dim<2, false, ROLE_UPDATE>(p, a, nseg, s);
