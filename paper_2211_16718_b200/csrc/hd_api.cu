@@ -350,7 +350,7 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
       });
     else
       rc = timed(p, HD_TK_SWEEP_Z, s, [&] {
-        return launch_sweep_update(p, us, inc, vflux, nullptr, scheme, stage, u, dt_dev, t, s);
+        return launch_sweep_update(p, us, inc, vflux, scheme, stage, u, dt_dev, t, s);
       });
   }
   return rc;

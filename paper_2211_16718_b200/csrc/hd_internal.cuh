@@ -125,7 +125,7 @@ int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int ac
 int launch_sweep_visc(const hd_plan* p, const double* u, double* inc, const double* vflux,
                       int64_t tag, cudaStream_t s);
 int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, const double* vflux,
-                        double* prim, int scheme, int stage, double* u, const double* dt_dev,
+                        int scheme, int stage, double* u, const double* dt_dev,
                         int64_t tag, cudaStream_t s);
 int launch_prims_planes(const hd_plan* p, const double* u, int z_lo, int z_hi, cudaStream_t s);
 int launch_fill_ghosts(const hd_plan* p, double* f, int nfields, int axis_mask, cudaStream_t s);

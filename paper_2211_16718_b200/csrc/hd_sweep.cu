@@ -345,7 +345,6 @@ struct SweepArgs {
   // ROLE_VISC / ROLE_UPDATE
   const double* vflux;  // 9 symmetric viscous flux fields (nullptr: inviscid)
   // ROLE_UPDATE
-  double* prim;         // primitives of the new stage state (nullptr: not needed)
   RKArgs rk;
 };
 
@@ -369,15 +368,6 @@ __device__ __forceinline__ bool line_of(const SweepArgs& a, int& i, int& j, int&
     k = 0;
     return i < G.n[0] && j < G.n[1];
   }
-}
-
-// The viscous primitives (u, v, w, T) of point (i, j, k) and their face images
-// along the locally periodic axes (the gradient stencils are axis-aligned).
-__device__ __forceinline__ void store_prim(double* prim, const Geo& G, int i, int j, int k,
-                                           const double (&pv)[4]) {
-  int64_t dl[6];
-  const int nd = face_image_deltas(G, i, j, k, periodic_mask(G), dl);
-  store_point_images<4>(prim, G.npts, G.idx(i, j, k), nd, dl, pv);
 }
 
 // PW: WENO power fixed at compile time (2, the reference default), or 0 = read
@@ -581,15 +571,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
           else ck = c - 1;
           double out[NV];
           rk_store_pre(a.rk, G, ci, cj, ck, val, ru0, racc, out);
-          if (a.prim) {
-            // viscous.py:80-81 primitives of the new state (u, v, w, T = gamma p / rho)
-            const double inv = frcp(out[0]);
-            double pv[4] = {out[1] * inv, out[2] * inv, out[3] * inv, 0.0};
-            const double p = gm1 * (out[4] - (0.5 * inv) * (out[1] * out[1] + out[2] * out[2] +
-                                                            out[3] * out[3]));
-            pv[3] = a.ph.gamma * p * inv;
-            store_prim(a.prim, G, ci, cj, ck, pv);
-          }
         } else {
 #pragma unroll
           for (int v = 0; v < NV; ++v) q[v * np] = val[v];
@@ -904,12 +885,11 @@ int launch_sweep_visc(const hd_plan* p, const double* u, double* inc, const doub
 }
 
 int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, const double* vflux,
-                        double* prim, int scheme, int stage, double* u, const double* dt_dev,
+                        int scheme, int stage, double* u, const double* dt_dev,
                         int64_t tag, cudaStream_t s) {
   int nseg;
   SweepArgs a = make_args(p, 2, u_stage, inc, 1, 0, tag, nseg);
   a.vflux = vflux;
-  a.prim = prim;
   a.rk = make_rk(p, scheme, stage, u, dt_dev);
   if (p->mode == HD_MODE_EXACT) return HD_E_UNSUPPORTED;  // exact mode runs the unfused stage
   return launch_dim<2, false, ROLE_UPDATE>(p, a, nseg, s);
