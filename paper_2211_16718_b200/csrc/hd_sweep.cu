@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
             const int o = r * SWEEP_THREADS;
             val[r + 1] += (8.0 * (p1[o] - m1[o]) + (m2[o] - p2[o])) * coef;
           }
-        } else if (VROLE && a.vflux) {  // direct stencil loads
+        } else if (!FWIN && VROLE && a.vflux) {  // direct stencil loads (no flux window)
           add_viscous_divergence<EXACT>(a.vflux, G, base + (int64_t)(c - 1) * sd,
                                         ROLE == ROLE_VISC ? 3 : 4, val);
         }
