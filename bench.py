@@ -124,6 +124,8 @@ def cpu_reference(n: int, steps: int, warmup: int, budget_s: float | None = None
     from paper_2211_16718_b200.hit import HitParams, synthesize_velocity
 
     O.lib()
+    # every host thread, even under torchrun (which exports OMP_NUM_THREADS=1)
+    O.set_num_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
     u, v, w = synthesize_velocity(n, HitParams(), "numpy")
     body = np.empty((5, n, n, n))
     body[0] = 1.0

@@ -524,3 +524,14 @@ int or_num_threads(void) {
   return 1;
 #endif
 }
+
+/* Thread count of the OpenMP loops (the reference arm uses every host thread even
+ * when a launcher such as torchrun exported OMP_NUM_THREADS=1). */
+void or_set_num_threads(int n) {
+#ifdef _OPENMP
+  extern void omp_set_num_threads(int);
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}

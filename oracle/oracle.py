@@ -149,6 +149,11 @@ def num_threads() -> int:
     return int(lib().or_num_threads())
 
 
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the oracle's loops (results are invariant to it)."""
+    lib().or_set_num_threads(int(n))
+
+
 def hyper_sweep(u, f, inc, npts, base0, sd, sa, sb, nd, nb, a_lo, a_hi, dim, inv_dx, gamma,
                 eps, power, delta):
     """kernels.py:68-73 signature; accumulates into ``inc``."""
