@@ -142,6 +142,12 @@ int hd_hyperbolic_rhs(hd_plan* plan, const double* u, double* inc, int accumulat
 
 /* viscous.py:54-121 parabolic_rhs: accumulates into inc rows 1..4. */
 int hd_parabolic_rhs(hd_plan* plan, const double* u, double* inc, void* stream);
+/* hd_parabolic_rhs in two halves around the flux-field halo of a decomposed
+ * block (viscous.py:111-120, the sync_scalars of RankHalo): the 9 symmetric
+ * viscous flux fields into HD_BUF_VFLUX (face images along the periodic axes),
+ * then inc[1..4] += their divergence in the reference order. */
+int hd_viscous_fluxes(hd_plan* plan, const double* u, void* stream);
+int hd_viscous_divergence(hd_plan* plan, double* inc, void* stream);
 
 /* kernels.py:207-227 central_diff4, same argument list. */
 int hd_central_diff4(const double* src, double* dst, int di, int dj, int dk, int g, int og,

@@ -42,7 +42,7 @@ EXPORTS = (
     "hd_error_read", "hd_error_clear", "hd_fp64_probe", "hd_bench_weights", "hd_launch_counter", "hd_timer_enable",
     "hd_timer_read", "hd_ipc_handle", "hd_ipc_open", "hd_ipc_close", "hd_peer_attach", "hd_peer_attach3", "hd_peer_signal",
     "hd_peer_wait", "hd_peer_timed_out", "hd_stage_buffer", "hd_rk4_step", "hd_max_signal",
-    "hd_totals", "hd_error_flags", "hd_halo_exchange",
+    "hd_totals", "hd_error_flags", "hd_halo_exchange", "hd_viscous_fluxes", "hd_viscous_divergence",
 )
 # hd_timer_read kinds (HD_TK_*)
 TIMER_KINDS = ("sweep_x", "sweep_y", "sweep_z", "gradflux", "prims", "divergence", "reduce")
@@ -121,6 +121,8 @@ def load(require_cuda: bool = False):
             "hd_launch_counter": ([], i64),
             "hd_stage_buffer": ([P, i32, i32, P, ctypes.POINTER(ctypes.c_void_p)], i32),
             "hd_rk4_step": ([P, P, P, P], i32),
+            "hd_viscous_fluxes": ([P, P, P], i32),
+            "hd_viscous_divergence": ([P, P, P], i32),
             "hd_max_signal": ([P, P, P, i32, P], i32),
             "hd_totals": ([P, P, P, P], i32),
             "hd_error_flags": ([P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64), P], i32),

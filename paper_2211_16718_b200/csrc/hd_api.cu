@@ -217,6 +217,22 @@ int hd_parabolic_rhs(hd_plan* p, const double* u, double* inc, void* stream) {
   return rc;
 }
 
+int hd_viscous_fluxes(hd_plan* p, const double* u, void* stream) {
+  if (!p || !u) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  if (p->phys.mu == 0.0) return HD_OK;
+  int rc = launch_prims(p, u, S(stream));
+  if (!rc) rc = launch_gradflux(p, nullptr, S(stream));
+  return rc;
+}
+
+int hd_viscous_divergence(hd_plan* p, double* inc, void* stream) {
+  if (!p || !inc) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  if (p->phys.mu == 0.0) return HD_OK;
+  return launch_divergence(p, 7, inc, inc, 0, HD_SCHEME_RK4, 0, nullptr, nullptr, S(stream));
+}
+
 int hd_rhs(hd_plan* p, double* u, double* inc, void* stream) {
   if (!p || !u || !inc) return HD_E_ARG;
   if (!p->ws) return HD_E_WORKSPACE;

@@ -285,6 +285,12 @@ class DistHalo:
         for arr in arrays:
             self._sync(arr.reshape(-1), 1, spec)
 
+    def sync_flux_fields(self, vflux: torch.Tensor, spec: GridSpec) -> None:
+        """The viscous flux groups' faces along the axes that differentiate them
+        (the sync_scalars of viscous.py:118 for a decomposed parabolic_rhs)."""
+        for d in self.split:
+            self.exchange_async(vflux, 9, spec, axes=(d,), fields=_VF_GROUP[d]).wait()
+
     # ---- fused march --------------------------------------------------------
     def advance(self, fields: FieldSet, gas: GasModel, tparams, weno_params: WenoParams,
                 delta: float, t0: float, observer, dt_provider, mode):

@@ -53,7 +53,16 @@ def parabolic_rhs(fields: FieldSet, gas: GasModel, halo=None, workers: int = 1,
         out = fields.like()
     if gas.effective_mu == 0.0:
         return out
-    if halo is not None and not getattr(halo, "periodic", (True, True, True)) == (True, True, True):
-        raise NotImplementedError("decomposed parabolic_rhs runs inside parallel_advance")
-    get_plan(fields.spec, gas, mode=mode).parabolic_rhs(fields.data, out.data)
+    periodic = tuple(getattr(halo, "periodic", (True, True, True))) if halo is not None else (True,) * 3
+    if periodic == (True, True, True):
+        get_plan(fields.spec, gas, mode=mode).parabolic_rhs(fields.data, out.data)
+        return out
+    # a decomposed block (DistHalo): fluxes, their faces along the split axes, divergence
+    from . import _lib
+    from .plan import _ptr, _stream_ptr
+
+    plan = get_plan(fields.spec, gas, mode=mode, periodic=periodic)
+    _lib.check(plan.L.hd_viscous_fluxes(plan.h, _ptr(fields.data), _stream_ptr()), "hd_viscous_fluxes")
+    halo.sync_flux_fields(plan.fields(_lib.HD_BUF_VFLUX, 9), fields.spec)
+    _lib.check(plan.L.hd_viscous_divergence(plan.h, _ptr(out.data), _stream_ptr()), "hd_viscous_divergence")
     return out

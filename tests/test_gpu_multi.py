@@ -321,3 +321,64 @@ def test_halo_exchange_entry_point_peer(tmp_path, dims):
     for r in range(2):
         with open(tmp_path / f"hx{r}.json") as fh:
             assert json.load(fh)["ok"], r
+
+
+RHS_SCRIPT = r'''
+import hashlib, json, os, sys
+sys.path.insert(0, os.environ["HD_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+import paper_2211_16718_b200 as hd
+rank = int(os.environ["RANK"]); world = int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(int(os.environ["LOCAL_RANK"]))
+dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ["LOCAL_RANK"])))
+dims = tuple(json.loads(os.environ["HD_DIMS"]))
+spec = hd.GridSpec((32, 32, 32))
+ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+gas = hd.GasModel(mu=0.006)
+lay = hd.decompose(spec, dims)[rank]
+local = hd.scatter(ic, [lay])[0]
+halo = hd.DistHalo(lay)
+inc = hd.make_rhs(gas, halo=halo, mode="exact")(local)
+parts = [torch.empty_like(inc.interior().contiguous()) for _ in range(world)]
+dist.all_gather(parts, inc.interior().contiguous())
+if rank == 0:
+    lays = hd.decompose(spec, dims)
+    locs = []
+    for r, part in enumerate(parts):
+        fs = hd.FieldSet.zeros(lays[r].spec)
+        fs.interior().copy_(part)
+        locs.append(fs)
+    glob = hd.gather(locs, lays, spec).interior().cpu().numpy()
+    with open(os.path.join(os.environ["HD_OUT"], "rhs.json"), "w") as fh:
+        json.dump({"sha": hashlib.sha256(np.ascontiguousarray(glob).tobytes()).hexdigest()}, fh)
+dist.destroy_process_group()
+'''
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 2), (2, 1, 1)])
+def test_decomposed_make_rhs_equals_monolithic(tmp_path, dims):
+    """make_rhs with a DistHalo (state faces, then the flux groups' faces between the
+    viscous fluxes and their divergence: viscous.py:111-120) equals the single-GPU
+    rhs bit-for-bit in exact mode."""
+    import hashlib
+
+    import numpy as np
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    import paper_2211_16718_b200 as hd
+
+    path = tmp_path / "rhs.py"
+    path.write_text(RHS_SCRIPT)
+    env = dict(os.environ, HD_ROOT=ROOT, HD_OUT=str(tmp_path), HD_DIMS=json.dumps(dims))
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node=2", "--master-addr=127.0.0.1", "--master-port=29549",
+                          str(path)], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    with open(tmp_path / "rhs.json") as fh:
+        multi = json.load(fh)
+    spec = hd.GridSpec((32, 32, 32))
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+    inc = hd.make_rhs(hd.GasModel(mu=0.006), mode="exact")(ic)
+    body = np.ascontiguousarray(inc.interior().cpu().numpy())
+    assert hashlib.sha256(body.tobytes()).hexdigest() == multi["sha"]
