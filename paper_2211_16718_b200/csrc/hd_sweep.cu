@@ -310,6 +310,9 @@ constexpr int SWEEP_THREADS = 64;
 #endif
 // z sweep (UPDATE role, flux window in the ring): 4 blocks/SM and up to 255
 // registers -- 9.7 -> 9.25 ms at 512^3 (6 blocks: spills; 4 without the window: 11.4)
+#ifndef HD_DX_PREFETCH
+#define HD_DX_PREFETCH 1  // L1 prefetch of the y sweep's D_x stencil: 8.05 -> 7.92 ms at 512^3
+#endif
 #ifndef HD_SWEEP_MIN_BLOCKS_Z
 #define HD_SWEEP_MIN_BLOCKS_Z 4
 #endif
@@ -490,6 +493,23 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
       if (c < c1) ffetch(c + 2);
     }
     const bool wr = c > c0;
+#if HD_DX_PREFETCH
+    // y sweep: pull the next cell's D_x stencil lines (x group) into L1 a window ahead
+    if constexpr (ROLE == ROLE_VISC) {
+      if (a.vflux && c < c1) {
+        const int64_t qn = base + (int64_t)c * sd;
+#pragma unroll
+        for (int r = 1; r < NV; ++r) {
+          const double* f = a.vflux + (int64_t)vf_field(0, r) * np + qn;
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(f));
+#if HD_DX_PREFETCH > 1
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(f - 2));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(f + 2));
+#endif
+        }
+      }
+    }
+#endif
     double* q = inc + (int64_t)(c - 1) * sd;
     // ROLE_UPDATE: the RK inputs of cell c-1 (base state, accumulator) are
     // loaded here, a full window of FP64 work before the update consumes them
