@@ -72,7 +72,8 @@ extern "C" {
 #define HD_BUF_ERR 7   /* error key (uint64) */
 #define HD_BUF_STATE 8 /* 5 fields: march state of a peer-attached plan (hd_peer_attach) */
 #define HD_BUF_SYNC 9  /* 16 uint64: peer flags [axis][state|vflux][from lo|hi], timeout word */
-#define HD_NBUF 10
+#define HD_BUF_FRED 10 /* per-warp partials of the diagnostics fused into the last z sweep */
+#define HD_NBUF 11
 
 /* results of hd_reduce_state (doubles at HD_BUF_RED result slot) */
 #define HD_RED_SIGNAL_MAX 0
@@ -176,6 +177,13 @@ int hd_stage_part(hd_plan* plan, int scheme, int stage, int parts, double* u,
 /* timeint.py:100-131: one pass over the interior producing HD_RED_* results
  * at `out` (device, HD_RED_N doubles).  Latches positivity (cons_to_prim). */
 int hd_reduce_state(hd_plan* plan, const double* u, double* out, int64_t tag, void* stream);
+
+/* Arm the diagnostics of the state the next completed step produces: the last
+ * RK stage's UPDATE (hd_step or hd_stage_part) writes the hd_reduce_state
+ * results of the new state to `out` with error tag `tag` -- folded into the z
+ * sweep in fast mode (no extra pass over the state), a separate reduction
+ * otherwise.  One-shot. */
+int hd_arm_reduce(hd_plan* plan, double* out, int64_t tag);
 
 /* timeint.py:133-138 + 224-237: ctx[DT] = cfl / signal (cfl > 0) or dt_fixed,
  * clipped to t_final - ctx[T] when t_final >= 0.  Latches a zero/non-finite

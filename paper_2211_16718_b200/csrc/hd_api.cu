@@ -49,7 +49,7 @@ void layout(const hd_geom* g, int64_t off[HD_NBUF], int64_t* total) {
   const int64_t f = npts_of(g) * 8;
   int64_t o = 0;
   const int64_t sizes[HD_NBUF] = {10 * f, 5 * f, 5 * f, 4 * f, 9 * f, RED_BYTES, 8 * HD_CTX_N, 64,
-                                  5 * f, 128};
+                                  5 * f, 128, fused_red_capacity(*g) * 9 * 8};
   for (int b = 0; b < HD_NBUF; ++b) {
     off[b] = o;
     o = align_up(o + sizes[b]);
@@ -358,6 +358,8 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   //   fast:  z sweep + D_z F_z + RK update
   if (!rc && (parts & HD_PART_UPDATE)) {
     if (!dt_dev) return HD_E_ARG;
+    const bool last = stage == nstages(scheme) - 1;
+    int fused = 0;
     // peer mode: the final stage's images land in the neighbours' HD_BUF_STATE
     if (p->geo.peer_any && u != buf(p, HD_BUF_STATE)) return HD_E_ARG;
     if (exact)
@@ -366,8 +368,13 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
       });
     else
       rc = timed(p, HD_TK_SWEEP_Z, s, [&] {
-        return launch_sweep_update(p, us, inc, vflux, scheme, stage, u, dt_dev, t, s);
+        return launch_sweep_update(p, us, inc, vflux, scheme, stage, u, dt_dev, t, s,
+                                   last ? p->red_out : nullptr, p->red_tag, &fused);
       });
+    // armed diagnostics of the step's result that the update could not fold in
+    if (!rc && last && p->red_out && !fused)
+      rc = timed(p, HD_TK_REDUCE, s, [&] { return launch_reduce(p, u, p->red_out, p->red_tag, s); });
+    if (last) p->red_out = nullptr;
   }
   return rc;
 }
@@ -386,6 +393,14 @@ int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag
     rc = hd_stage_part(p, scheme, st, HD_PART_ALL, u, dt_dev, tag, stream);
   }
   return rc;
+}
+
+int hd_arm_reduce(hd_plan* p, double* out, int64_t tag) {
+  if (!p) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  p->red_out = out;
+  p->red_tag = tag;
+  return HD_OK;
 }
 
 int hd_stage_buffer(hd_plan* p, int scheme, int stage, double* u, void** out) {

@@ -62,6 +62,35 @@ __device__ __forceinline__ int periodic_mask(const Geo& G) {
          ((G.periodic[2] || G.peer[2]) ? 4 : 0);
 }
 
+__device__ __forceinline__ double dmax_nan(double a, double b) {
+  // numpy max propagates NaN
+  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(a, b);
+}
+
+// Fast-mode diagnostics of one conserved state (timeint.py:100-131 with one
+// reciprocal of rho): folds it into acc = {signal max, signal sum, wavespeed,
+// mass, mx, my, mz, energy, KE}; returns 1 / 2 for a nonpositive density /
+// pressure, else 0.  Shared by reduce_kernel<fast> and the fused z sweep.
+__device__ __forceinline__ int diag_fast(const double (&c)[5], double gamma, double rh0, double rh1,
+                                         double rh2, double (&acc)[9]) {
+  const double rho = c[0], m1 = c[1], m2 = c[2], m3 = c[3], E = c[4];
+  const double inv = frcp(rho);
+  const double v0 = m1 * inv, v1 = m2 * inv, v2 = m3 * inv;
+  const double p = (gamma - 1.0) * (E - (0.5 * inv) * (m1 * m1 + m2 * m2 + m3 * m3));
+  const double a = sqrt(gamma * p * inv);
+  const double s0 = (fabs(v0) + a) * rh0, s1 = (fabs(v1) + a) * rh1, s2 = (fabs(v2) + a) * rh2;
+  acc[0] = dmax_nan(acc[0], dmax_nan(dmax_nan(s0, s1), s2));
+  acc[1] = dmax_nan(acc[1], (s0 + s1) + s2);
+  acc[2] = dmax_nan(acc[2], dmax_nan(dmax_nan(fabs(v0), fabs(v1)), fabs(v2)) + a);
+  acc[3] += rho;
+  acc[4] += m1;
+  acc[5] += m2;
+  acc[6] += m3;
+  acc[7] += E;
+  acc[8] += 0.5 * ((v0 * v0 + v1 * v1) + v2 * v2);
+  return !(rho > 0.0) ? 1 : (!(p > 0.0) ? 2 : 0);
+}
+
 // does the point (i,j,k) have a face image that lands in a neighbour's buffer?
 __device__ __forceinline__ bool touches_peer(const Geo& G, int i, int j, int k) {
   const int g = G.g;

@@ -520,11 +520,6 @@ __global__ void central_diff4_kernel(const double* __restrict__ src, double* __r
 constexpr int RED_BLOCKS_MAX = 2048;
 constexpr int RED_THREADS = 256;
 
-__device__ __forceinline__ double dmax_nan(double a, double b) {
-  // numpy max propagates NaN
-  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000LL) : fmax(a, b);
-}
-
 // EXACT: the reference's true divisions and sqrt (dt bitwise equal to the
 // reference); fast: one reciprocal of rho and multiplications by 1/h (dt within
 // a few ulp)
@@ -617,6 +612,18 @@ __global__ void reduce_finish_kernel(const double* partial, int nblocks, double*
   }
   if (lane == 0)
     for (int c = 0; c < 9; ++c) out[c] = vals[c];
+}
+
+int launch_reduce_finish(const double* partial, int nparts, double* out, cudaStream_t s) {
+  reduce_finish_kernel<<<1, 32, 0, s>>>(partial, nparts, out);
+  hd::count_launches(1);
+  return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+}
+
+int64_t fused_red_capacity(const hd_geom& g) {
+  // z-sweep warps: (n_x / 32) x n_y lines x segments (make_args caps them at n_z / 8)
+  const int64_t seg = g.n[2] / 8 > 1 ? g.n[2] / 8 : 1;
+  return (int64_t)((g.n[0] + 31) / 32) * g.n[1] * seg;
 }
 
 int launch_reduce(const hd_plan* p, const double* u, double* out, int64_t tag, cudaStream_t s) {

@@ -112,6 +112,8 @@ struct hd_plan {
   void* timer;  // per-kernel event timer (hd_timer_enable), owned
   char* peer_lo[3];  // neighbours' workspaces mapped here (hd_peer_attach3), not owned
   char* peer_hi[3];
+  double* red_out;   // armed diagnostics of the next step's result (hd_arm_reduce)
+  int64_t red_tag;
 };
 
 namespace hd {
@@ -124,9 +126,15 @@ int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int ac
 // z viscous divergence + RK update + primitives of the new stage state
 int launch_sweep_visc(const hd_plan* p, const double* u, double* inc, const double* vflux,
                       int64_t tag, cudaStream_t s);
+// red_out != nullptr on the last stage: fold the diagnostics of the new state
+// in when possible (*fused = 1), else the caller reduces separately
 int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, const double* vflux,
                         int scheme, int stage, double* u, const double* dt_dev,
-                        int64_t tag, cudaStream_t s);
+                        int64_t tag, cudaStream_t s, double* red_out = nullptr, int64_t red_tag = 0,
+                        int* fused = nullptr);
+int launch_reduce_finish(const double* partial, int nparts, double* out, cudaStream_t s);
+// partial slots of HD_BUF_FRED (one per z-sweep warp of the segment heuristic)
+int64_t fused_red_capacity(const hd_geom& g);
 int launch_prims_planes(const hd_plan* p, const double* u, int z_lo, int z_hi, cudaStream_t s);
 int launch_fill_ghosts(const hd_plan* p, double* f, int nfields, int axis_mask, cudaStream_t s);
 int launch_prims(const hd_plan* p, const double* u, cudaStream_t s);

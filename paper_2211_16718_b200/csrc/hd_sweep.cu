@@ -332,7 +332,10 @@ template <int DIM> struct SweepCfg {
 //               images (into the z neighbours' ghost planes in peer mode)
 // The flux group differentiated along the sweep rides in the shared ring with the
 // window (one HBM read per value); the y sweep reads D_x's stencil directly.
-constexpr int ROLE_PLAIN = 0, ROLE_VISC = 1, ROLE_UPDATE = 2;
+// ROLE_UPDATE_DIAG: ROLE_UPDATE of the last stage with the diagnostics of the new
+// state folded in (hd_arm_reduce) -- a separate instantiation, so the other stages'
+// update kernel carries none of its registers
+constexpr int ROLE_PLAIN = 0, ROLE_VISC = 1, ROLE_UPDATE = 2, ROLE_UPDATE_DIAG = 3;
 
 struct SweepArgs {
   Geo geo;
@@ -349,6 +352,11 @@ struct SweepArgs {
   const double* vflux;  // 9 symmetric viscous flux fields (nullptr: inviscid)
   // ROLE_UPDATE
   RKArgs rk;
+  // ROLE_UPDATE, last stage: diagnostics of the new state fused in (nullptr: off);
+  // one partial (HD_RED_* layout) per warp
+  double* fred;
+  int64_t fred_tag;
+  double rh[3];  // 1 / h
 };
 
 // Line geometry: thread -> interior coords of the line origin
@@ -408,9 +416,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   // z 9.7 -> 9.25 ms at 512^3 with the z sweep at 4 blocks/SM; 1 = y only,
   // 2 = z only, 0 = stencil read directly from HBM/L1)
   constexpr bool VROLE = ROLE != ROLE_PLAIN;
+  constexpr bool UPD = ROLE == ROLE_UPDATE || ROLE == ROLE_UPDATE_DIAG;
+  constexpr bool DIAG = ROLE == ROLE_UPDATE_DIAG && !EXACT;
   constexpr bool FWIN = VROLE && (HD_SWEEP_FLUX_WINDOW == 3 ||
                                   (HD_SWEEP_FLUX_WINDOW == 1 && ROLE == ROLE_VISC) ||
-                                  (HD_SWEEP_FLUX_WINDOW == 2 && ROLE == ROLE_UPDATE));
+                                  (HD_SWEEP_FLUX_WINDOW == 2 && UPD));
   constexpr int RV = FWIN ? 13 : 9;  // values per ring slot
   __shared__ double ring[SMEM_WINDOW ? 5 * RV * SWEEP_THREADS : 1];
   double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
@@ -473,6 +483,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   }
 
   double lu[NV], lf[NV];  // left states at c-1/2 (carried)
+  // fused diagnostics of the new state (ROLE_UPDATE, last stage)
+  double diag[9] = {-INFINITY, -INFINITY, -INFINITY, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   double fprev[NV];
   for (int c = c0 - 1; c <= c1; ++c) {
     // shift; position c+2 enters from the prefetch buffer
@@ -514,7 +526,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
     // ROLE_UPDATE: the RK inputs of cell c-1 (base state, accumulator) are
     // loaded here, a full window of FP64 work before the update consumes them
     double ru0[NV], racc[NV];
-    if constexpr (ROLE == ROLE_UPDATE) {
+    if constexpr (UPD) {
       const int64_t qo = base + (int64_t)(c - 1) * sd;
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
@@ -584,13 +596,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
         if constexpr (ROLE == ROLE_VISC) {
 #pragma unroll
           for (int v = 0; v < NV; ++v) q[v * np] = val[v];
-        } else if constexpr (ROLE == ROLE_UPDATE) {
+        } else if constexpr (UPD) {
           int ci = li, cj = lj, ck = lk;
           if (DIM == 0) ci = c - 1;
           else if (DIM == 1) cj = c - 1;
           else ck = c - 1;
           double out[NV];
           rk_store_pre(a.rk, G, ci, cj, ck, val, ru0, racc, out);
+          if constexpr (DIAG) {
+            const int code = diag_fast(out, a.ph.gamma, a.rh[0], a.rh[1], a.rh[2], diag);
+            if (code) latch_error(a.err, a.fred_tag, code, G.idx(ci, cj, ck));
+          }
         } else {
 #pragma unroll
           for (int v = 0; v < NV; ++v) q[v * np] = val[v];
@@ -605,8 +621,24 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
       lf[v] = nf[v];
     }
   }
+  if constexpr (DIAG) {
+    // deterministic warp tree; one partial per warp (the launcher guarantees full warps)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) diag[c] = dmax_nan(diag[c], __shfl_down_sync(0xffffffffu, diag[c], off));
+#pragma unroll
+      for (int c = 3; c < 9; ++c) diag[c] += __shfl_down_sync(0xffffffffu, diag[c], off);
+    }
+    if (threadIdx.x == 0) {
+      const int64_t w = ((int64_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) *
+                            blockDim.y + threadIdx.y;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) a.fred[w * 9 + c] = diag[c];
+    }
+  }
   // peer stores (this line segment held boundary planes) performed before the kernel ends
-  if (ROLE == ROLE_UPDATE && DIM == 2 && G.peer_any &&
+  if (UPD && DIM == 2 && G.peer_any &&
       ((G.peer[2] && (c0 < G.g || c1 > nd - G.g)) || touches_peer(G, li, lj, G.g)))
     __threadfence_system();
 }
@@ -906,12 +938,27 @@ int launch_sweep_visc(const hd_plan* p, const double* u, double* inc, const doub
 
 int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, const double* vflux,
                         int scheme, int stage, double* u, const double* dt_dev,
-                        int64_t tag, cudaStream_t s) {
+                        int64_t tag, cudaStream_t s, double* red_out, int64_t red_tag, int* fused) {
   int nseg;
   SweepArgs a = make_args(p, 2, u_stage, inc, 1, 0, tag, nseg);
   a.vflux = vflux;
   a.rk = make_rk(p, scheme, stage, u, dt_dev);
   if (p->mode == HD_MODE_EXACT) return HD_E_UNSUPPORTED;  // exact mode runs the unfused stage
+  // the last stage can fold the diagnostics of the new state in (hd_arm_reduce):
+  // full warps only (n_x % 32, n_y % 2), and room for one partial per warp
+  const Geo& G = p->geo;
+  const int64_t warps = (int64_t)(G.n[0] / 32) * G.n[1] * nseg;
+  if (fused) *fused = 0;
+  if (red_out && a.rk.to_u && G.n[0] % 32 == 0 && G.n[1] % 2 == 0 &&
+      warps <= fused_red_capacity(p->geom)) {
+    a.fred = (double*)(p->ws + p->off[HD_BUF_FRED]);
+    a.fred_tag = red_tag;
+    for (int d = 0; d < 3; ++d) a.rh[d] = 1.0 / G.h[d];
+    int rc = launch_dim<2, false, ROLE_UPDATE_DIAG>(p, a, nseg, s);
+    if (!rc) rc = launch_reduce_finish(a.fred, (int)warps, red_out, s);
+    if (!rc && fused) *fused = 1;
+    return rc;
+  }
   return launch_dim<2, false, ROLE_UPDATE>(p, a, nseg, s);
 }
 

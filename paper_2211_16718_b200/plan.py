@@ -163,6 +163,11 @@ class Plan:
         _lib.check(self.L.hd_reduce_state(self.h, _ptr(u), _ptr(out), tag, _stream_ptr()),
                    "hd_reduce_state")
 
+    def arm_reduce(self, out, tag: int) -> None:
+        """The next completed step also writes the diagnostics of its result to
+        ``out`` (fused into the last z sweep in fast mode; hd_arm_reduce)."""
+        _lib.check(self.L.hd_arm_reduce(self.h, _ptr(out), tag), "hd_arm_reduce")
+
     def set_dt(self, red, cfl_mode: int, cfl: float, dt_fixed: float, t_final: float, ctx,
                tag: int) -> None:
         _lib.check(self.L.hd_set_dt(self.h, _ptr(red) if red is not None else ctypes.c_void_p(None),

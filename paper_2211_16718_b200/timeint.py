@@ -355,9 +355,10 @@ class _DeviceMarch:
             plan.set_dt(None, 0, 0.0, tp.dt, -1.0, self.ctx, tag * 8)
         else:
             plan.set_dt(self.red, cfl_mode, tp.cfl, 0.0, -1.0, self.ctx, tag * 8)
+        plan.arm_reduce(self.red, tag * 8 + 7)  # diagnostics of the new state (= next CFL signal)
         self.stepper(self.out.data, self.ctx[_lib.HD_CTX_DT:], tag)
         plan.commit_time(self.ctx)
-        self._reduce(tag * 8 + 7)  # diagnostics of the new state = next step's CFL signal
+        self.reducer(self.red)
 
     def _run_graph(self) -> AdvanceResult:
         """max_steps without host synchronisation, the steps replayed from CUDA
@@ -451,9 +452,12 @@ class _DeviceMarch:
                 if not have_signal:
                     self._reduce(tag_pre)
                 plan.set_dt(self.red, cfl_mode, tp.cfl, 0.0, t_final, self.ctx, tag_pre)
+            # diagnostics of the new state (= next step's CFL signal), fused into the last
+            # RK stage's update kernel when the plan can (hd_arm_reduce)
+            plan.arm_reduce(self.red, step * 8 + 7)
             self.stepper(self.out.data, self.ctx[_lib.HD_CTX_DT:], step)
             plan.commit_time(self.ctx)
-            self._reduce(step * 8 + 7)  # diagnostics of the new state = next step's CFL signal
+            self.reducer(self.red)
             have_signal = True
             recs.push(self.ctx, self.red)
             step += 1
