@@ -285,6 +285,7 @@ def advance(fields, gas: GasModel, tparams: TimeParams, weno_params: WenoParams 
     input is not modified except for its ghost layers (as the reference's
     rhs refills them in place).
     """
+    uploaded = isinstance(fields, FieldSet) and not fields.data.is_cuda
     fields = _as_device(fields)
     if fields.layout != Layout.COMPONENT_CONTIGUOUS:
         raise ValueError("advance needs COMPONENT_CONTIGUOUS fields")
@@ -296,7 +297,8 @@ def advance(fields, gas: GasModel, tparams: TimeParams, weno_params: WenoParams 
                                 mode)
         raise TypeError(f"unsupported halo {type(halo).__name__}")
     plan = get_plan(fields.spec, gas, weno_params, delta, mode)
-    runner = _DeviceMarch(plan, fields, gas, tparams, t0)
+    # a freshly uploaded host state is ours to march in place (no second device copy)
+    runner = _DeviceMarch(plan, fields, gas, tparams, t0, copy=not uploaded)
     return runner.run(observer, dt_provider)
 
 
