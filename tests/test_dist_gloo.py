@@ -1,4 +1,5 @@
-"""Host-side multi-rank logic on CPU with the gloo backend (world size 2 and 4).
+"""Host-side multi-rank logic on CPU with the gloo backend (world size 2, 4 and 8 —
+the (1, 1, 8) z slabs bench.py uses on 8 GPUs).
 
 The NCCL path on the GPU uses exactly this code (DistHalo) on CUDA tensors;
 here the z-slab halo protocol is checked against the monolithic periodic
@@ -87,7 +88,7 @@ def _worker(rank, world, port, n, q, dims):
 
 
 @pytest.mark.parametrize("dims", [(1, 1, 2), (1, 1, 4), (2, 1, 1), (1, 2, 1), (2, 2, 1), (1, 2, 2),
-                                  (2, 1, 2)])
+                                  (2, 1, 2), (1, 1, 8)])
 def test_block_halo_matches_monolithic_wrap(dims):
     """Every 3D block decomposition (decomp.py:66-103): after sync_fields each
     rank's ghosted block, edges and corners included, equals the periodic
