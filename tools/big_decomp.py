@@ -1,0 +1,102 @@
+"""The paper's largest grid, decomposed: 1024^3 as z slabs over the ranks of
+one box (4 GPUs: 1024 x 1024 x 256 per GPU, ~96 GB of workspace + state each;
+the BASELINE config runs it on 8), RK4 (CFL 0.3: see --cfl), fast mode, peer-store halo.
+
+Each rank fills its own slab with a smooth, periodic, solenoidal-velocity state
+evaluated on global coordinates (the HIT synthesis needs a global 1024^3 FFT
+that would not leave room for the workspace; the step cost does not depend on
+the data: no branches with delta = 0).  Checks: finite, global mass conserved.
+
+    torchrun --nproc-per-node 4 tools/big_decomp.py [--grid 1024] [--steps 100] [--warmup 3]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2211_16718_b200 as hd  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--grid", type=int, default=1024)
+ap.add_argument("--steps", type=int, default=100)
+ap.add_argument("--warmup", type=int, default=3)
+# The reference's dt is convective only (timeint.py:122-138).  With mu = 0.006 the
+# 4th-order viscous/heat-conduction operator (D4 applied twice: |k* h|^2 <= 1.883 per
+# axis; diffusivity gamma mu / Pr = 0.0117) is RK4-stable only for dt <= 2.785 h^2 /
+# (3 * 1.883 * 0.0117) = 42 h^2: at 1024^3 that is 1.59e-3 while CFL 0.4 gives 1.8e-3,
+# and the march stops with StepError (nonpositive pressure) after ~80 steps; CFL 0.3 is stable.
+ap.add_argument("--cfl", type=float, default=0.3)
+a = ap.parse_args()
+
+rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+local = int(os.environ.get("LOCAL_RANK", 0))
+torch.cuda.set_device(local)
+os.environ.setdefault("TORCH_NCCL_HIGH_PRIORITY", "1")
+dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+n = a.grid
+spec = hd.GridSpec((n, n, n))
+lay = hd.decompose(spec, (1, 1, world))[rank]
+fs = hd.FieldSet.zeros(lay.spec)
+it = fs.interior()
+h = 2 * math.pi / n
+oz = lay.offset[2]
+lz = lay.local_n[2]
+z = (oz + torch.arange(lz, dtype=torch.float64, device="cuda"))[:, None, None] * h
+y = torch.arange(n, dtype=torch.float64, device="cuda")[None, :, None] * h
+x = torch.arange(n, dtype=torch.float64, device="cuda")[None, None, :] * h
+# Taylor-Green-like velocity (divergence-free) plus a k = 4 perturbation, rho = 1, p = 1/gamma
+u0 = 0.3
+it[0] = 1.0
+it[1] = u0 * torch.sin(x) * torch.cos(y) * torch.cos(z) + 0.05 * torch.sin(4 * y) * torch.cos(4 * z)
+it[2] = -u0 * torch.cos(x) * torch.sin(y) * torch.cos(z) + 0.05 * torch.sin(4 * z) * torch.cos(4 * x)
+it[3] = 0.05 * torch.sin(4 * x) * torch.cos(4 * y)
+it[4] = (1.0 / 1.4) / 0.4 + 0.5 * (it[1] ** 2 + it[2] ** 2 + it[3] ** 2)
+del x, y, z
+torch.cuda.empty_cache()
+gas = hd.GasModel(mu=0.006)
+halo = hd.DistHalo(lay)
+
+
+def march(state, steps):
+    tp = hd.TimeParams(scheme="rk4", cfl=a.cfl, max_steps=steps)
+    return halo.advance(state, gas, tp, hd.DEFAULT_PARAMS, 0.0, 0.0, None, None, None)
+
+
+def mass(state):
+    t = state.interior()[0].sum().reshape(1) * lay.spec.cell_volume()
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+m0 = mass(fs)
+res = march(fs, a.warmup)
+dist.barrier()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+res = march(res.fields, a.steps)
+e1.record()
+dist.barrier()
+torch.cuda.synchronize()
+ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+ms = float(ms.item())
+fin = torch.tensor([float(torch.isfinite(res.fields.interior()).all())], device="cuda")
+dist.all_reduce(fin, op=dist.ReduceOp.MIN)
+m1 = mass(res.fields)
+peak = torch.tensor([torch.cuda.max_memory_allocated() / 1e9], dtype=torch.float64, device="cuda")
+dist.all_reduce(peak, op=dist.ReduceOp.MAX)
+if rank == 0:
+    out = {"grid": [n, n, n], "n_gpus": world, "dims": [1, 1, world], "steps": a.steps, "cfl": a.cfl,
+           "warmup": a.warmup, "ms_per_step": ms / a.steps,
+           "pt_step_per_s": n ** 3 * a.steps / (ms / 1e3), "t": res.t,
+           "finite": bool(fin.item() == 1.0), "mass_rel_change": abs(m1 - m0) / abs(m0),
+           "peak_mem_gb_max_rank": float(peak.item()),
+           "peer_halo": any(l.digests is not None for l in hd.decomp._PeerLink._cache.values())}
+    print(json.dumps(out))
+dist.destroy_process_group()
