@@ -23,6 +23,9 @@ import paper_2211_16718_b200 as hd  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--grid", type=int, default=1024)
+ap.add_argument("--nz", type=int, default=0, help="global z extent (default: --grid); e.g. "
+                "512 x 512 x 256 on 4 GPUs gives each the 64-plane slab of 512^3 on 8")
+ap.add_argument("--dims", default="", help="block shape x,y,z (default 1,1,world)")
 ap.add_argument("--steps", type=int, default=100)
 ap.add_argument("--warmup", type=int, default=3)
 # The reference's dt is convective only (timeint.py:122-138).  With mu = 0.006 the
@@ -39,16 +42,21 @@ torch.cuda.set_device(local)
 os.environ.setdefault("TORCH_NCCL_HIGH_PRIORITY", "1")
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 n = a.grid
-spec = hd.GridSpec((n, n, n))
-lay = hd.decompose(spec, (1, 1, world))[rank]
+nz = a.nz or n
+spec = hd.GridSpec((n, n, nz), (2 * math.pi, 2 * math.pi, 2 * math.pi * nz / n))
+dims = tuple(int(v) for v in a.dims.split(",")) if a.dims else (1, 1, world)
+lay = hd.decompose(spec, dims)[rank]
 fs = hd.FieldSet.zeros(lay.spec)
 it = fs.interior()
 h = 2 * math.pi / n
-oz = lay.offset[2]
+ox, oy, oz = lay.offset
+ly = lay.local_n[1]
+lx = lay.local_n[0]
 lz = lay.local_n[2]
-z = (oz + torch.arange(lz, dtype=torch.float64, device="cuda"))[:, None, None] * h
-y = torch.arange(n, dtype=torch.float64, device="cuda")[None, :, None] * h
-x = torch.arange(n, dtype=torch.float64, device="cuda")[None, None, :] * h
+# one period over the z extent (the box is 2 pi nz / n long; the spacing stays h)
+z = (oz + torch.arange(lz, dtype=torch.float64, device="cuda"))[:, None, None] * (2 * math.pi / nz)
+y = (oy + torch.arange(ly, dtype=torch.float64, device="cuda"))[None, :, None] * h
+x = (ox + torch.arange(lx, dtype=torch.float64, device="cuda"))[None, None, :] * h
 # Taylor-Green-like velocity (divergence-free) plus a k = 4 perturbation, rho = 1, p = 1/gamma
 u0 = 0.3
 it[0] = 1.0
@@ -92,9 +100,9 @@ m1 = mass(res.fields)
 peak = torch.tensor([torch.cuda.max_memory_allocated() / 1e9], dtype=torch.float64, device="cuda")
 dist.all_reduce(peak, op=dist.ReduceOp.MAX)
 if rank == 0:
-    out = {"grid": [n, n, n], "n_gpus": world, "dims": [1, 1, world], "steps": a.steps, "cfl": a.cfl,
+    out = {"grid": [n, n, nz], "n_gpus": world, "dims": list(dims), "steps": a.steps, "cfl": a.cfl,
            "warmup": a.warmup, "ms_per_step": ms / a.steps,
-           "pt_step_per_s": n ** 3 * a.steps / (ms / 1e3), "t": res.t,
+           "pt_step_per_s": n * n * nz * a.steps / (ms / 1e3), "t": res.t,
            "finite": bool(fin.item() == 1.0), "mass_rel_change": abs(m1 - m0) / abs(m0),
            "peak_mem_gb_max_rank": float(peak.item()),
            "peer_halo": any(l.digests is not None for l in hd.decomp._PeerLink._cache.values())}

@@ -1,4 +1,4 @@
-# tools/big_decomp.py across sizes / rank counts / halo paths / CFL (diagnosis matrix)
+# tools/big_decomp.py across sizes / rank counts / halo paths / CFL / block shapes (diagnosis matrix)
 p=29600
 run() {  # label nproc env args...
   local label=$1 np=$2 envs=$3; shift 3
@@ -8,6 +8,6 @@ run() {  # label nproc env args...
   echo "$label rc=$? $(grep -h '^{' gpurun_out/bm_$label.log | tail -1) $(grep -h -m1 'StepError' gpurun_out/bm_$label.log | cut -c1-200)" >> gpurun_out/bm.txt
 }
 rm -f gpurun_out/bm.txt
-run s1024n4 4 HD_PEER=1 --grid 1024 --steps 100 --cfl 0.3
-run s1024n4cfl4 4 HD_PEER=1 --grid 1024 --steps 100 --cfl 0.4
-run s1024n4nccl 4 HD_PEER=0 --grid 1024 --steps 20 --cfl 0.3
+run s512z256d114 4 HD_PEER=1 --grid 512 --nz 256 --steps 30 --cfl 0.4 --dims 1,1,4
+run s512z256d122 4 HD_PEER=1 --grid 512 --nz 256 --steps 30 --cfl 0.4 --dims 1,2,2
+run s512z256d212 4 HD_PEER=1 --grid 512 --nz 256 --steps 30 --cfl 0.4 --dims 2,1,2
