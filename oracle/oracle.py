@@ -101,11 +101,12 @@ def _p(a: np.ndarray):
 class OracleStateError(ValueError):
     """Nonpositive density (code 1) or pressure (code 2) met by the oracle."""
 
-    def __init__(self, code: int, where: int, stage: int | None = None):
+    def __init__(self, code: int, where: int, stage: int | None = None, step: int | None = None):
         kind = {1: "density", 2: "pressure"}.get(code, f"code {code}")
         super().__init__(f"nonpositive {kind} at flat point {where}" +
-                         (f" in stage {stage}" if stage is not None else ""))
-        self.code, self.where, self.stage = code, where, stage
+                         (f" in stage {stage}" if stage is not None else "") +
+                         (f" of step {step}" if step is not None else ""))
+        self.code, self.where, self.stage, self.step = code, where, stage, step
 
 
 @dataclass(frozen=True)
@@ -227,7 +228,9 @@ def advance(u: np.ndarray, prob: Problem, steps: int, cfl: float | None = 0.4,
                           float(cfl or 0.0), float(dt or 0.0), int(steps), _p(dts),
                           ctypes.byref(where))
     if rc:
-        raise OracleStateError(rc % 10, where.value, stage=(rc // 10) % 10)
+        # steps 1..k-1 completed; step k stored its dt unless its CFL reduction failed (rc >= 100)
+        k = int(np.count_nonzero(dts)) + (1 if rc >= 100 else 0)
+        raise OracleStateError(rc % 10, where.value, stage=(rc // 10) % 10, step=k)
     return dts[:steps]
 
 

@@ -36,6 +36,12 @@ def traj32_golden():
 
 
 @pytest.fixture(scope="session")
+def viscous_limit_golden():
+    with open(os.path.join(GOLDEN, "viscous_limit.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="session")
 def oracle():
     from oracle import oracle as O
 

@@ -23,6 +23,9 @@ Fixtures (tests/golden/):
                 canonical values of bench.make_bench_values
   traj32.json   config 1 (32^3, RK4, CFL 0.4, mu=0.006, 10 steps): IC and
                 final SHA-256, per-variable L2, dts, KE per step
+  viscous_limit.json  16^3 HIT, RK4, CFL 0.4 at mu = 0.3 (dt beyond the viscous
+                operator's RK4 limit): the StepError step / stage / kind the
+                reference raises; at mu = 0.2: 60 steps complete, final t and dts
 """
 
 from __future__ import annotations
@@ -172,6 +175,24 @@ def trajectory32():
     print(json.dumps(doc, indent=1))
 
 
+def viscous_limit():
+    n = 16
+    spec = hd.GridSpec((n, n, n))
+    ic = hd.make_initial_condition(spec, hd.HitParams())
+    doc = {"n": n, "cfl": 0.4, "scheme": "rk4", "max_steps": 60}
+    try:
+        hd.advance(ic, hd.GasModel(mu=0.3), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=60))
+        raise SystemExit("expected StepError at mu = 0.3")
+    except hd.StepError as e:
+        doc["unstable"] = {"mu": 0.3, "step": int(e.step), "stage": int(e.stage),
+                           "message": str(e)}
+    r = hd.advance(ic, hd.GasModel(mu=0.2), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=60))
+    doc["stable"] = {"mu": 0.2, "steps": len(r.records), "t": r.t,
+                     "dts": [rec.dt for rec in r.records]}
+    with open(os.path.join(OUT, "viscous_limit.json"), "w") as fh:
+        json.dump(doc, fh, indent=1)
+
+
 def bench_weights():
     from hitdns import bench
 
@@ -191,7 +212,11 @@ if __name__ == "__main__":
     if _sys.argv[1:] == ["bench_weights"]:
         bench_weights()
         raise SystemExit(0)
+    if _sys.argv[1:] == ["viscous_limit"]:
+        viscous_limit()
+        raise SystemExit(0)
     bench_weights()
     kernel_vectors()
     trajectory16()
     trajectory32()
+    viscous_limit()

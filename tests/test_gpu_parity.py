@@ -205,6 +205,37 @@ def test_step_error_reports_stage(hd):
     assert ei.value.step == 1 and ei.value.stage == 1
 
 
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_viscous_time_step_limit_fails_like_the_reference(hd, viscous_limit_golden, mode):
+    """The reference's dt is convective only (timeint.py:122-138); when the
+    viscosity makes the fourth-order viscous operator RK4-unstable at that dt
+    (dt > ~42 h^2 at mu = 0.006, i.e. n >~ 900; here n = 16 with mu = 0.3) the
+    march grows the highest modes until a pressure goes negative.  The GPU march
+    must stop at the step and stage the reference stops at
+    (tests/golden/viscous_limit.json; exact mode: the same trajectory, bit for
+    bit; fast mode: within one step), and the stable viscosity must run through
+    (exact mode: the reference's dt sequence)."""
+    G = viscous_limit_golden
+    n = G["n"]
+    spec = hd.GridSpec((n,) * 3)
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+    bad, ok = G["unstable"], G["stable"]
+    with pytest.raises(hd.StepError) as ge:
+        hd.advance(ic, hd.GasModel(mu=bad["mu"]),
+                   hd.TimeParams(scheme="rk4", cfl=G["cfl"], max_steps=G["max_steps"]), mode=mode)
+    assert ge.value.stage == bad["stage"]
+    assert "pressure" in str(ge.value)
+    if mode == "exact":
+        assert ge.value.step == bad["step"]
+    else:
+        assert abs(ge.value.step - bad["step"]) <= 1
+    res = hd.advance(ic, hd.GasModel(mu=ok["mu"]),
+                     hd.TimeParams(scheme="rk4", cfl=G["cfl"], max_steps=G["max_steps"]), mode=mode)
+    assert res.steps == G["max_steps"]
+    if mode == "exact":
+        assert [r.dt for r in res.records] == ok["dts"]
+
+
 def test_uniform_flow_zero_rhs(hd):
     n = 12
     spec = hd.GridSpec((n, n, n))
