@@ -18,5 +18,6 @@ for spec in "$@"; do
   done
   wait
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libhd.so $out/*.o -lcudart
+  rm -f $out/*.o  # only the .so travels to the GPU box (gpurun snapshot limit)
   echo "$name: $(grep -c spill $out/hd_sweep.ptxas.log) kernels, spills: $(grep 'spill' $out/hd_sweep.ptxas.log | grep -v ' 0 bytes spill stores' | wc -l)"
 done
