@@ -1,3 +1,4 @@
+# Round-end check on one 4-GPU box: GPU test suite, bench at N = 1, 2, 4 and the reference arm -> gpurun_out/final_*
 set -x
 python -m pytest tests -m gpu -q -x > gpurun_out/final_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/final_tests.log
 python bench.py > gpurun_out/final_n1.json 2> gpurun_out/final_n1.err

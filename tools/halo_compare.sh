@@ -1,3 +1,4 @@
+# 4-GPU bench with the NVLink peer-store halo vs the NCCL halo (HD_PEER=0): per-kernel times -> gpurun_out/mg.txt
 timeout 600 python -m pytest tests/test_gpu_multi.py -q -x -k "decomposed or scale" > gpurun_out/multi.log 2>&1
 p=29640
 for cfg in "HD_PEER=1" "HD_PEER=0"; do
