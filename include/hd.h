@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define HD_ABI_VERSION 2
+#define HD_ABI_VERSION 3
 
 /* status codes */
 #define HD_OK 0
@@ -56,10 +56,12 @@ extern "C" {
 #define HD_PART_UPDATE 8  /* fast: z sweep + D_z F_z + RK update;
                              exact: viscous divergence + RK update */
 #define HD_PART_ALL 15
-#define HD_PART_PRIMS 16  /* accepted, no effect (ABI 1 compatibility) */
 
-/* hd_step flags */
-#define HD_STEP_PRIMS_VALID 1 /* accepted, no effect (ABI 1 compatibility) */
+/* plan options (hd_plan_set_option); results never depend on them (tests) */
+#define HD_OPT_SEGMENTS 0      /* sweep segments per line: 0 = automatic (>= 6 waves), else fixed */
+#define HD_OPT_X_STAGED 1      /* 1 (default): cp.async-staged x sweep when n_y % 32 == 0; 0: plain */
+#define HD_OPT_FLUX_ZMARCH 2   /* 1 (default): z-marching viscous flux kernel when the tiles fit; 0: pointwise */
+#define HD_OPT_N 3
 
 /* workspace buffers (hd_plan_buffer) */
 #define HD_BUF_STAGE 0 /* 10 fields: RK stage states, ping-pong halves (stage s writes half s%2) */
@@ -122,6 +124,8 @@ int64_t hd_workspace_bytes(const hd_geom* geom);
 int hd_plan_create(const hd_geom* geom, const hd_gas* gas, const hd_weno* weno, int mode,
                    void* workspace, int64_t workspace_bytes, hd_plan** out);
 int hd_plan_destroy(hd_plan* plan);
+/* Set a kernel-selection option (HD_OPT_*) of a plan; applies to later launches. */
+int hd_plan_set_option(hd_plan* plan, int option, int64_t value);
 /* Device pointer of a workspace buffer (HD_BUF_*). */
 void* hd_plan_buffer(hd_plan* plan, int which);
 int64_t hd_plan_total_points(const hd_plan* plan);
@@ -163,8 +167,7 @@ int hd_rhs(hd_plan* plan, double* u, double* inc, void* stream);
  * place, dt read from device memory.  Ghosts of u must be valid on entry and
  * are valid on exit (locally periodic axes).  `tag` identifies the step in
  * the error key. */
-int hd_step(hd_plan* plan, int scheme, double* u, const double* dt_dev, int64_t tag, int flags,
-            void* stream);
+int hd_step(hd_plan* plan, int scheme, double* u, const double* dt_dev, int64_t tag, void* stream);
 
 /* One part of one RK stage (decomposed runs).  Stage s reads u (s == 0) or
  * half (s-1)%2 of the workspace STAGE buffer; the UPDATE part writes the next

@@ -22,8 +22,8 @@ HD_MODE_FAST = 0
 HD_MODE_EXACT = 1
 HD_SCHEME_RK3 = 3
 HD_SCHEME_RK4 = 4
-HD_PART_LOCAL, HD_PART_HALO, HD_PART_MID, HD_PART_UPDATE, HD_PART_ALL, HD_PART_PRIMS = 1, 2, 4, 8, 15, 16
-HD_STEP_PRIMS_VALID = 1
+HD_PART_LOCAL, HD_PART_HALO, HD_PART_MID, HD_PART_UPDATE, HD_PART_ALL = 1, 2, 4, 8, 15
+HD_OPT_SEGMENTS, HD_OPT_X_STAGED, HD_OPT_FLUX_ZMARCH = 0, 1, 2
 (HD_BUF_STAGE, HD_BUF_ACC, HD_BUF_INC, HD_BUF_PRIM, HD_BUF_VFLUX, HD_BUF_RED, HD_BUF_CTX,
  HD_BUF_ERR, HD_BUF_STATE, HD_BUF_SYNC, HD_BUF_FRED) = range(11)
 HD_PEER_STATE, HD_PEER_VFLUX = 0, 1
@@ -36,7 +36,7 @@ HD_CTX_N = 4
 # every symbol include/hd.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "hd_abi_version", "hd_status_string", "hd_workspace_bytes", "hd_plan_create",
-    "hd_plan_destroy", "hd_plan_buffer", "hd_plan_total_points", "hd_fill_ghosts",
+    "hd_plan_destroy", "hd_plan_set_option", "hd_plan_buffer", "hd_plan_total_points", "hd_fill_ghosts",
     "hd_hyper_sweep", "hd_hyperbolic_rhs", "hd_parabolic_rhs", "hd_central_diff4", "hd_rhs",
     "hd_step", "hd_stage_part", "hd_reduce_state", "hd_set_dt", "hd_commit_time",
     "hd_error_read", "hd_error_clear", "hd_fp64_probe", "hd_bench_weights", "hd_launch_counter", "hd_timer_enable",
@@ -109,7 +109,8 @@ def load(require_cuda: bool = False):
             "hd_parabolic_rhs": ([P, P, P, P], i32),
             "hd_central_diff4": ([P, P] + [i32] * 10 + [f64, P], i32),
             "hd_rhs": ([P, P, P, P], i32),
-            "hd_step": ([P, i32, P, P, i64, i32, P], i32),
+            "hd_step": ([P, i32, P, P, i64, P], i32),
+            "hd_plan_set_option": ([P, i32, i64], i32),
             "hd_stage_part": ([P, i32, i32, i32, P, P, i64, P], i32),
             "hd_reduce_state": ([P, P, P, i64, P], i32),
             "hd_set_dt": ([P, P, i32, f64, f64, f64, P, i64, P], i32),

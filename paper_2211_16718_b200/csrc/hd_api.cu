@@ -160,6 +160,9 @@ int hd_plan_create(const hd_geom* geom, const hd_gas* gas, const hd_weno* weno, 
   ph.delta = weno->delta;
   p->ws = (char*)workspace;
   p->ws_bytes = workspace_bytes;
+  p->opt[HD_OPT_SEGMENTS] = 0;
+  p->opt[HD_OPT_X_STAGED] = 1;
+  p->opt[HD_OPT_FLUX_ZMARCH] = 1;
   std::memcpy(p->off, off, sizeof(off));
   if (cudaGetDevice(&p->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {
@@ -179,6 +182,12 @@ int hd_plan_create(const hd_geom* geom, const hd_gas* gas, const hd_weno* weno, 
 int hd_plan_destroy(hd_plan* p) {
   if (p) timer_free(p->timer);
   delete p;
+  return HD_OK;
+}
+
+int hd_plan_set_option(hd_plan* p, int option, int64_t value) {
+  if (!p || option < 0 || option >= HD_OPT_N || value < 0) return HD_E_ARG;
+  p->opt[option] = value;
   return HD_OK;
 }
 
@@ -336,8 +345,6 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
     if (!rc && exact)
       rc = timed(p, HD_TK_SWEEP_Y, s, [&] { return launch_sweep(p, 1, us, inc, 1, 0, t, s); });
   }
-  // PRIMS: kept for ABI compatibility; no kernel (the fast gradflux derives
-  // the primitives from the state itself, exact mode makes them in HALO)
   // HALO (reads every ghost of `us`)
   //   exact: z sweep, primitives of the whole box, viscous fluxes
   //   fast:  viscous fluxes straight from the state (primitives on the fly)
@@ -379,9 +386,7 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   return rc;
 }
 
-int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag, int flags,
-            void* stream) {
-  (void)flags;  // HD_STEP_PRIMS_VALID: no effect since ABI 1
+int hd_step(hd_plan* p, int scheme, double* u, const double* dt_dev, int64_t tag, void* stream) {
   if (!p || !u || !dt_dev) return HD_E_ARG;
   if (!p->ws) return HD_E_WORKSPACE;
   if (scheme != HD_SCHEME_RK3 && scheme != HD_SCHEME_RK4) return HD_E_ARG;

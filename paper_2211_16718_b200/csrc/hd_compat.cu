@@ -41,7 +41,7 @@ using namespace hd;
 extern "C" {
 
 int hd_rk4_step(hd_plan* p, double* u, const double* dt_dev, void* stream) {
-  return hd_step(p, HD_SCHEME_RK4, u, dt_dev, 0, 0, stream);
+  return hd_step(p, HD_SCHEME_RK4, u, dt_dev, 0, stream);
 }
 
 int hd_max_signal(hd_plan* p, const double* u, double* out_dev, int mode, void* stream) {

@@ -9,8 +9,6 @@
 //   rk_update_kernel     timeint.py:168-193 when mu == 0 (viscous.py:72-73 short-circuit)
 //   central_diff4_kernel kernels.py:207-227 (stand-alone, for the operator API)
 //   reduce kernels       timeint.py:100-131 (CFL signal, totals, max wavespeed, KE)
-#include <cstdlib>
-
 #include "hd_device.cuh"
 
 namespace hd {
@@ -207,19 +205,8 @@ __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict_
 // a per-thread register queue of 5 planes (each prims value is loaded once per
 // column), the x/y stencils from a shared-memory plane tile with a 2-point halo.
 // Needs n_x % 32 == 0 and n_y % 8 == 0 (else gradflux_kernel).
-#ifndef HD_GZ_MINB
-#define HD_GZ_MINB 2
-#endif
-#ifndef HD_GZ_WAVES
-#define HD_GZ_WAVES 4
-#endif
-#ifndef HD_GZ_TX
-#define HD_GZ_TX 32
-#endif
-#ifndef HD_GZ_TY
-#define HD_GZ_TY 8
-#endif
-constexpr int GZ_TX = HD_GZ_TX, GZ_TY = HD_GZ_TY, GZ_H = 2;
+// 32 x 8 tiles, 2 blocks/SM, ~4 waves (32x16 and 16x16 tiles measured slower)
+constexpr int GZ_TX = 32, GZ_TY = 8, GZ_H = 2, GZ_MINB = 2, GZ_WAVES = 4;
 constexpr int GZ_PX = GZ_TX + 2 * GZ_H, GZ_PY = GZ_TY + 2 * GZ_H;
 
 // fast-mode viscous primitives (u, v, w, T) from the 5 conserved values (the
@@ -237,7 +224,7 @@ __device__ __forceinline__ void prims_of(const double (&c)[5], double gamma, dou
 // converted to primitives on the fly (no primitive fields in HBM); else `src`
 // holds the 4 primitive fields.
 template <bool EXACT, bool FROM_U>
-__global__ void __launch_bounds__(GZ_TX * GZ_TY, HD_GZ_MINB) gradflux_zm_kernel(
+__global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_zm_kernel(
     const double* __restrict__ prim, double* __restrict__ vf, Geo G, double mu, double q_coef,
     int zseg, double gamma) {
   // two plane tiles (double-buffered: one barrier per plane); every load is
@@ -383,10 +370,10 @@ int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s) {
   double* vf = (double*)(p->ws + p->off[HD_BUF_VFLUX]);
   const double mu = p->phys.mu;
   const double q_coef = (-mu) / ((p->phys.gamma - 1.0) * p->phys.prandtl);  // viscous.py:107
-  if (G.n[0] % GZ_TX == 0 && G.n[1] % GZ_TY == 0 && !getenv("HD_NO_GZ")) {
+  if (G.n[0] % GZ_TX == 0 && G.n[1] % GZ_TY == 0 && p->opt[HD_OPT_FLUX_ZMARCH]) {
     // z segments: enough blocks for ~4 waves of 2 blocks per SM
     const int64_t cols = (int64_t)(G.n[0] / GZ_TX) * (G.n[1] / GZ_TY);
-    int nseg = (int)((p->sm_count * HD_GZ_MINB * HD_GZ_WAVES + cols - 1) / cols);
+    int nseg = (int)((p->sm_count * GZ_MINB * GZ_WAVES + cols - 1) / cols);
     nseg = nseg < 1 ? 1 : (nseg > G.n[2] ? G.n[2] : nseg);
     const int zseg = (G.n[2] + nseg - 1) / nseg;
     nseg = (G.n[2] + zseg - 1) / zseg;

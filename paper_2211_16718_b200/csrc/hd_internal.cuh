@@ -49,13 +49,9 @@ __device__ __forceinline__ double frcp(double x) {
 // scales the correction term sum_k w_k (c_k - q2) (recon_pair), so its relative
 // error (~1e-14) enters the reconstructed value scaled by |c_k - q2| / |q2|.
 __device__ __forceinline__ double frcp_weights(double x) {
-#ifdef HD_WEIGHT_RCP_NEWTON2
-  return frcp(x);
-#else
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
   return fma(r, fma(-x, r, 1.0), r);
-#endif
 }
 
 // Geometry of one plan, passed by value to every kernel.
@@ -114,6 +110,7 @@ struct hd_plan {
   char* peer_hi[3];
   double* red_out;   // armed diagnostics of the next step's result (hd_arm_reduce)
   int64_t red_tag;
+  int64_t opt[HD_OPT_N];  // hd_plan_set_option
 };
 
 namespace hd {

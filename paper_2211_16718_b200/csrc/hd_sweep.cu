@@ -17,7 +17,6 @@
 // inc read-modify-write is a fully coalesced 256-byte warp access.
 // x sweep: lanes are consecutive y rows; each lane walks its row sequentially
 // (sector reuse through L1).
-#include <cstdlib>
 #include <cstring>
 
 #include "hd_device.cuh"
@@ -296,30 +295,14 @@ constexpr int SWEEP_THREADS = 64;
 //         <= 168 registers, no spills) -- 7.3 ms vs 8.3 ms with a register window
 //   x:    register window, 4 blocks per SM -- its lanes walk different rows, and
 //         more resident warps thrash L1 (15.5 ms at 6 blocks vs 9.9 ms)
-#ifndef HD_SWEEP_SMEM_WINDOW_YZ
-#define HD_SWEEP_SMEM_WINDOW_YZ 1
-#endif
-#ifndef HD_SWEEP_MIN_BLOCKS_YZ
-#define HD_SWEEP_MIN_BLOCKS_YZ 6
-#endif
-#ifndef HD_SWEEP_MIN_BLOCKS_X
-#define HD_SWEEP_MIN_BLOCKS_X 4
-#endif
-#ifndef HD_SWEEP_FLUX_WINDOW
-#define HD_SWEEP_FLUX_WINDOW 3
-#endif
-// z sweep (UPDATE role, flux window in the ring): 4 blocks/SM and up to 255
+// x: 4 blocks/SM with a register window; y: 6 blocks/SM with the window in the
+// shared ring; z (UPDATE role, flux window in the ring): 4 blocks/SM and up to 255
 // registers -- 9.7 -> 9.25 ms at 512^3 (6 blocks: spills; 4 without the window: 11.4)
-#ifndef HD_DX_PREFETCH
-#define HD_DX_PREFETCH 1  // L1 prefetch of the y sweep's D_x stencil: 8.05 -> 7.92 ms at 512^3
-#endif
-#ifndef HD_SWEEP_MIN_BLOCKS_Z
-#define HD_SWEEP_MIN_BLOCKS_Z 4
-#endif
+constexpr int SWEEP_MIN_BLOCKS_X = 4, SWEEP_MIN_BLOCKS_Y = 6, SWEEP_MIN_BLOCKS_Z = 4;
 template <int DIM> struct SweepCfg {
-  static constexpr bool smem_window = DIM != 0 && HD_SWEEP_SMEM_WINDOW_YZ;
+  static constexpr bool smem_window = DIM != 0;
   static constexpr int min_blocks =
-      DIM == 0 ? HD_SWEEP_MIN_BLOCKS_X : (DIM == 1 ? HD_SWEEP_MIN_BLOCKS_YZ : HD_SWEEP_MIN_BLOCKS_Z);
+      DIM == 0 ? SWEEP_MIN_BLOCKS_X : (DIM == 1 ? SWEEP_MIN_BLOCKS_Y : SWEEP_MIN_BLOCKS_Z);
 };
 
 // What a sweep does besides -dF/dx (the fast-mode stage pipeline, hd_api.cu):
@@ -412,15 +395,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   // The VISC/UPDATE roles append 4 columns: the viscous flux group F_dim
   // (differentiated along the sweep) at the same positions, so D_dim F_dim
   // reads each flux value from HBM once.
-  // (HD_SWEEP_FLUX_WINDOW: 3 = both roles, the default -- y 8.28 -> 8.06 ms,
-  // z 9.7 -> 9.25 ms at 512^3 with the z sweep at 4 blocks/SM; 1 = y only,
-  // 2 = z only, 0 = stencil read directly from HBM/L1)
+  // (y 8.28 -> 8.06 ms, z 9.7 -> 9.25 ms at 512^3 against stencil loads)
   constexpr bool VROLE = ROLE != ROLE_PLAIN;
   constexpr bool UPD = ROLE == ROLE_UPDATE || ROLE == ROLE_UPDATE_DIAG;
   constexpr bool DIAG = ROLE == ROLE_UPDATE_DIAG && !EXACT;
-  constexpr bool FWIN = VROLE && (HD_SWEEP_FLUX_WINDOW == 3 ||
-                                  (HD_SWEEP_FLUX_WINDOW == 1 && ROLE == ROLE_VISC) ||
-                                  (HD_SWEEP_FLUX_WINDOW == 2 && UPD));
+  constexpr bool FWIN = VROLE;
   constexpr int RV = FWIN ? 13 : 9;  // values per ring slot
   __shared__ double ring[SMEM_WINDOW ? 5 * RV * SWEEP_THREADS : 1];
   double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
@@ -505,23 +484,16 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
       if (c < c1) ffetch(c + 2);
     }
     const bool wr = c > c0;
-#if HD_DX_PREFETCH
-    // y sweep: pull the next cell's D_x stencil lines (x group) into L1 a window ahead
+    // y sweep: pull the next cell's D_x stencil lines (x group) into L1 a window
+    // ahead (8.05 -> 7.92 ms at 512^3)
     if constexpr (ROLE == ROLE_VISC) {
       if (a.vflux && c < c1) {
         const int64_t qn = base + (int64_t)c * sd;
 #pragma unroll
-        for (int r = 1; r < NV; ++r) {
-          const double* f = a.vflux + (int64_t)vf_field(0, r) * np + qn;
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(f));
-#if HD_DX_PREFETCH > 1
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(f - 2));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(f + 2));
-#endif
-        }
+        for (int r = 1; r < NV; ++r)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.vflux + (int64_t)vf_field(0, r) * np + qn));
       }
     }
-#endif
     double* q = inc + (int64_t)(c - 1) * sd;
     // ROLE_UPDATE: the RK inputs of cell c-1 (base state, accumulator) are
     // loaded here, a full window of FP64 work before the update consumes them
@@ -589,9 +561,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
             const int o = r * SWEEP_THREADS;
             val[r + 1] += (8.0 * (p1[o] - m1[o]) + (m2[o] - p2[o])) * coef;
           }
-        } else if (!FWIN && VROLE && a.vflux) {  // direct stencil loads (no flux window)
-          add_viscous_divergence<EXACT>(a.vflux, G, base + (int64_t)(c - 1) * sd,
-                                        ROLE == ROLE_VISC ? 3 : 4, val);
         }
         if constexpr (ROLE == ROLE_VISC) {
 #pragma unroll
@@ -652,38 +621,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
 // l%4: four full 32-byte sectors per instruction), double-buffered one chunk
 // ahead, and its increments go out the same way through a staging tile.
 // ---------------------------------------------------------------------------
-static bool getenv_flag(const char* name) {
-  const char* v = getenv(name);
-  return v && v[0] && v[0] != '0';
-}
-
-// Chunk of XC positions per row; staging tiles have row pitch XC + 1 doubles
-// (odd: conflict-free 64-bit access).  XC <= 2 would leave room for a
-// shared-memory window ring (as in the y/z sweeps) but measured slower at
-// 512^3 (149-165 vs 141 ms/step): XC = 4 with a register window.
-#ifndef HD_XCHUNK
-#define HD_XCHUNK 4
-#endif
-constexpr int XC = HD_XCHUNK;
-#ifndef HD_XPAD
-#define HD_XPAD (HD_XCHUNK + 1)
-#endif
-#ifndef HD_XOUT_STAGE
-#define HD_XOUT_STAGE 1
-#endif
-constexpr int XS_PAD = HD_XPAD;
-constexpr bool XOUT_STAGE = HD_XOUT_STAGE;
-constexpr bool XRING = XC <= 2;
-constexpr int XMINB = XRING ? HD_SWEEP_MIN_BLOCKS_YZ : HD_SWEEP_MIN_BLOCKS_X;
+// Chunks of XC = 4 positions per row; staging tiles have row pitch XC + 1
+// doubles (odd: conflict-free 64-bit access).  Chunks of 2 with a shared-memory
+// window ring measured slower at 512^3 (149-165 vs 141 ms/step).
+constexpr int XC = 4;
+constexpr int XS_PAD = XC + 1;
 
 template <bool EXACT, int PW>
-__global__ void __launch_bounds__(SWEEP_THREADS, XMINB) sweep_x_staged_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_staged_kernel(const SweepArgs a) {
   constexpr int WARPS = SWEEP_THREADS / 32;
   __shared__ double xin[WARPS][2][NV][32 * XS_PAD];
-  __shared__ double xout[XOUT_STAGE ? WARPS : 1][NV][32 * XS_PAD];
-  __shared__ double ring[XRING ? 5 * 9 * SWEEP_THREADS : 1];
-  double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
-  auto slot = [&](int m) -> double* { return mine + ((m + 5) % 5) * (9 * SWEEP_THREADS); };
+  __shared__ double xout[WARPS][NV][32 * XS_PAD];
   const Geo& G = a.geo;
   const int lane = threadIdx.x, w = threadIdx.y;
   const int j0 = blockIdx.x * 32;  // launch guarantees n_y % 32 == 0
@@ -726,13 +674,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS, XMINB) sweep_x_staged_kernel(co
     for (int v = 0; v < NV; ++v) uu[v] = s[v * 32 * XS_PAD];
     double inv, pv[4];
     point_flux<0, EXACT>(uu, gm1, ff, inv, pv);
-    if constexpr (XRING) {
-      double* sp = slot(p);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) sp[v * SWEEP_THREADS] = uu[v];
-#pragma unroll
-      for (int v = 1; v < NV; ++v) sp[(NV - 1 + v) * SWEEP_THREADS] = ff[v];
-    }
     if (a.check && p >= 0 && p < nd) {
       if (!(uu[0] > 0.0)) latch_error(a.err, a.tag, 1, base + p);
       else if (!(pv[3] > 0.0)) latch_error(a.err, a.tag, 2, base + p);
@@ -783,39 +724,21 @@ __global__ void __launch_bounds__(SWEEP_THREADS, XMINB) sweep_x_staged_kernel(co
       __syncwarp();
       issue((p - p0) / XC + 1);
     }
-    if constexpr (!XRING) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          wu[q][v] = wu[q + 1][v];
-          wf[q][v] = wf[q + 1][v];
-        }
-    }
+      for (int v = 0; v < NV; ++v) {
+        wu[q][v] = wu[q + 1][v];
+        wf[q][v] = wf[q + 1][v];
+      }
     take(p, wu[4], wf[4]);
     double ru[NV], rf[NV], nu[NV], nf[NV];
-    if constexpr (XRING) {
-      const double* w0 = slot(c - 2);
-      const double* w1 = slot(c - 1);
-      const double* w2 = slot(c);
-      const double* w3 = slot(c + 1);
-      const double* w4 = slot(c + 2);
 #pragma unroll
-      for (int v = 0; v < 2 * NV - 1; ++v) {
-        double l, r;
-        recon_pair<EXACT>(w0[v * SWEEP_THREADS], w1[v * SWEEP_THREADS], w2[v * SWEEP_THREADS],
-                          w3[v * SWEEP_THREADS], w4[v * SWEEP_THREADS], eps, power, l, r);
-        if (v < NV) { nu[v] = l; ru[v] = r; }
-        else { nf[v - NV + 1] = l; rf[v - NV + 1] = r; }
-      }
-    } else {
+    for (int v = 0; v < NV; ++v)
+      recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
 #pragma unroll
-      for (int v = 0; v < NV; ++v)
-        recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
-#pragma unroll
-      for (int v = 1; v < NV; ++v)
-        recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
-    }
+    for (int v = 1; v < NV; ++v)
+      recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
     nf[0] = nu[1];
     rf[0] = ru[1];
     if (c >= c0) {
@@ -829,16 +752,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, XMINB) sweep_x_staged_kernel(co
           double d;
           if constexpr (EXACT) d = xm(xs(flux[v], fprev[v]), a.inv_dx);
           else d = (flux[v] - fprev[v]) * a.inv_dx;
-          if constexpr (XOUT_STAGE) {
-            xout[w][v][lane * XS_PAD + oo] = d;
-          } else {
-            double* dst = a.inc + base + m + v * np;
-            const double old = a.accumulate ? *dst : 0.0;
-            if constexpr (EXACT) *dst = xs(old, d);
-            else *dst = old - d;
-          }
+          xout[w][v][lane * XS_PAD + oo] = d;
         }
-        if (XOUT_STAGE && (oo == XC - 1 || m == c1 - 1)) flush((m - c0) / XC);
+        if (oo == XC - 1 || m == c1 - 1) flush((m - c0) / XC);
       }
 #pragma unroll
       for (int v = 0; v < NV; ++v) fprev[v] = flux[v];
@@ -884,17 +800,12 @@ static SweepArgs make_args(const hd_plan* p, int dim, const double* u, double* i
   a.tag = tag;
   // segment length: enough independent lines to fill ~6 waves of 148 SMs x 256 threads
   const int64_t lines = (int64_t)G.n[0] * G.n[1] * G.n[2] / G.n[dim];
-#ifndef HD_SWEEP_WAVES
-#define HD_SWEEP_WAVES 6
-#endif
-  const int64_t target = (int64_t)p->sm_count * 256 * HD_SWEEP_WAVES;
+  const int64_t target = (int64_t)p->sm_count * 256 * 6;
   nseg = (int)((target + lines - 1) / lines);
   if (nseg < 1) nseg = 1;
   if (nseg > G.n[dim] / 8) nseg = G.n[dim] / 8 > 0 ? G.n[dim] / 8 : 1;
-  if (const char* e = getenv("HD_SWEEP_SEGMENTS")) {  // tests: results must not depend on it
-    const int want = atoi(e);
-    if (want >= 1 && want <= G.n[dim]) nseg = want;
-  }
+  // HD_OPT_SEGMENTS (tests: results must not depend on the split)
+  if (p->opt[HD_OPT_SEGMENTS] >= 1 && p->opt[HD_OPT_SEGMENTS] <= G.n[dim]) nseg = (int)p->opt[HD_OPT_SEGMENTS];
   a.seg = (G.n[dim] + nseg - 1) / nseg;
   nseg = (G.n[dim] + a.seg - 1) / a.seg;
   return a;
@@ -906,7 +817,7 @@ int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int ac
   int nseg;
   SweepArgs a = make_args(p, dim, u, inc, accumulate, check, tag, nseg);
   const bool exact = p->mode == HD_MODE_EXACT;
-  if (dim == 0 && p->geo.n[1] % 32 == 0 && !getenv_flag("HD_NO_XSTAGE")) {
+  if (dim == 0 && p->geo.n[1] % 32 == 0 && p->opt[HD_OPT_X_STAGED]) {
     constexpr int BY = SWEEP_THREADS / 32;
     const Geo& G = p->geo;
     dim3 block(32, BY, 1), grid(G.n[1] / 32, (G.n[2] + BY - 1) / BY, nseg);

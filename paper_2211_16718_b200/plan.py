@@ -150,9 +150,13 @@ class Plan:
     def rhs(self, u, inc) -> None:
         _lib.check(self.L.hd_rhs(self.h, _ptr(u), _ptr(inc), _stream_ptr()), "hd_rhs")
 
-    def step(self, scheme: int, u, dt_dev, tag: int, flags: int = 0) -> None:
-        _lib.check(self.L.hd_step(self.h, scheme, _ptr(u), _ptr(dt_dev), tag, flags, _stream_ptr()),
-                   "hd_step")
+    def step(self, scheme: int, u, dt_dev, tag: int) -> None:
+        _lib.check(self.L.hd_step(self.h, scheme, _ptr(u), _ptr(dt_dev), tag, _stream_ptr()), "hd_step")
+
+    def set_option(self, option: int, value: int) -> None:
+        """Kernel selection (HD_OPT_*): sweep segments per line, staged x sweep,
+        z-marching flux kernel.  Results never depend on it."""
+        _lib.check(self.L.hd_plan_set_option(self.h, option, int(value)), "hd_plan_set_option")
 
     def stage_part(self, scheme: int, stage: int, parts: int, u, dt_dev, tag: int) -> None:
         _lib.check(self.L.hd_stage_part(self.h, scheme, stage, parts, _ptr(u),

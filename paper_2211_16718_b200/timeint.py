@@ -324,7 +324,7 @@ class _DeviceMarch:
         self.scheme = _SCHEME_CODE[tparams.scheme]
         # multi-rank drivers override how a step runs and how reductions combine
         self.own_stepper = stepper is None and reducer is None
-        self.stepper = stepper or (lambda u, dt_dev, tag: plan.step(self.scheme, u, dt_dev, tag, 0))
+        self.stepper = stepper or (lambda u, dt_dev, tag: plan.step(self.scheme, u, dt_dev, tag))
         self.reducer = reducer or (lambda red: None)
         self.error_combine = error_combine or (lambda key: key)
 

@@ -30,7 +30,7 @@ def test_library_exports_every_symbol():
     missing = [s for s in _declared() if not hasattr(L, s)]
     assert not missing
     lib = _lib.load()
-    assert lib.hd_abi_version() == 2
+    assert lib.hd_abi_version() == 3
     assert lib.hd_status_string(-4) == b"unsupported configuration"
 
 

@@ -100,12 +100,13 @@ def test_segment_split_invariance(hd, monkeypatch, mode):
     p = torch.from_numpy(0.8 + 0.4 * rng.random(shape)).cuda()
     fs = _from_prims(hd, spec, rho, *vel, p)
     outs = []
-    for segs in ("1", "4", "7"):
-        monkeypatch.setenv("HD_SWEEP_SEGMENTS", segs)
+    for segs in (1, 4, 7):
         hd.release_plans()
+        hd.get_plan(spec, hd.GasModel(mu=0.01), mode=mode).set_option(hd._lib.HD_OPT_SEGMENTS, segs)
         res = hd.advance(fs, hd.GasModel(mu=0.01), hd.TimeParams(scheme="rk4", cfl=0.3, max_steps=2),
                          mode=mode)
         outs.append(res.fields.interior().cpu().numpy())
+    hd.release_plans()
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 

@@ -292,12 +292,13 @@ def test_x_sweep_staged_matches_unstaged(hd, oracle, monkeypatch, mode):
     u = oracle.from_interior(body, P)
     fs = _fs(hd, P, u)
     outs = []
-    for flag in ("0", "1"):
-        monkeypatch.setenv("HD_NO_XSTAGE", flag)
+    for staged in (1, 0):
+        hd.get_plan(fs.spec, hd.GasModel(), mode=mode).set_option(hd._lib.HD_OPT_X_STAGED, staged)
         inc = fs.like()
         inc.data.fill_(0.25)
         hd.hyper_sweep(fs, 0, inc, mode=mode)
         outs.append(inc.numpy())
+    hd.get_plan(fs.spec, hd.GasModel(), mode=mode).set_option(hd._lib.HD_OPT_X_STAGED, 1)
     if mode == "exact":
         assert np.array_equal(outs[0], outs[1])
     else:  # different kernels may contract FMAs differently
