@@ -1,7 +1,7 @@
 """Benchmark: grid-point RK4-step updates/s (fp64) of the HIT decay problem.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--n 512] [--mode fast|exact]
-    python bench.py --impl reference ...        # the CPU reference arm (C oracle port)
+    python bench.py --impl reference ...        # the CPU reference arm (hitdns itself)
 
 One step = what the reference's ``advance`` does per step (timeint.py:224-257):
 CFL dt (global max reduction), one classical RK4 step (4 x [ghost sync,
@@ -116,8 +116,48 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def host_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def reference_cpu(n: int, steps: int, warmup: int, budget_s: float | None = None):
+    """The unmodified reference package (hitdns 0.1.0 from baseline/_ref, numba
+    kernels) through its public API: ``hitdns.advance(..., workers=<host threads>)``
+    one RK4 step per call (CFL dt, stepper, diagnostics: timeint.py:199-258) on
+    its own n^3 HIT IC.  None when the package (or numba) is not importable."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "hd_numba_cache"))
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import hitdns
+    except ImportError:
+        return None
+    workers = host_threads()
+    ic = hitdns.make_initial_condition(hitdns.GridSpec((n, n, n)), hitdns.HitParams())
+    gas = hitdns.GasModel(mu=MU)
+    one = hitdns.TimeParams(scheme="rk4", cfl=0.4, max_steps=1)
+    fields, t = ic, 0.0
+    for _ in range(max(warmup, 1)):  # the first call also JIT-compiles the numba kernels
+        r = hitdns.advance(fields, gas, one, workers=workers, t0=t)
+        fields, t = r.fields, r.t
+    t0 = time.perf_counter()
+    done = 0
+    while done < steps:
+        r = hitdns.advance(fields, gas, one, workers=workers, t0=t)
+        fields, t = r.fields, r.t
+        done += 1
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    return n ** 3 * done / el, done, el, workers
+
+
 def cpu_reference(n: int, steps: int, warmup: int, budget_s: float | None = None):
-    """The C oracle port of the reference path (OpenMP, all host threads)."""
+    """The C oracle port of the reference path (OpenMP, all host threads): the
+    fallback CPU baseline when the reference package is not installed."""
     import numpy as np
 
     from oracle import oracle as O
@@ -125,7 +165,7 @@ def cpu_reference(n: int, steps: int, warmup: int, budget_s: float | None = None
 
     O.lib()
     # every host thread, even under torchrun (which exports OMP_NUM_THREADS=1)
-    O.set_num_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+    O.set_num_threads(host_threads())
     u, v, w = synthesize_velocity(n, HitParams(), "numpy")
     body = np.empty((5, n, n, n))
     body[0] = 1.0
@@ -159,21 +199,46 @@ def workload_config(args, world: int, dims=None) -> dict:
             "ic": "HIT (HitParams defaults) synthesised on the GPU (torch backend)"}
 
 
+def cpu_baseline(n: int, steps: int, warmup: int, budget_s: float, metric_n: int = 512):
+    """(rate, steps done, seconds, threads, kind, sample text, config overrides):
+    the reference package itself when installed (kind "reference"), else the C port."""
+    got = reference_cpu(n, steps, warmup, budget_s)
+    if got is not None:
+        rate, done, el, threads = got
+        return rate, done, el, threads, "reference", (
+            f"hitdns 0.1.0 (the unmodified reference, baseline/_ref) hitdns.advance(..., "
+            f"workers={threads}) on its own {n}^3 HIT IC, RK4 CFL 0.4 mu {MU}: {done} steps in "
+            f"{el:.1f} s after {max(warmup, 1)} warm-up (numba JIT)"), {
+                "grid": n, "parallelism": f"CPU, {threads} host threads (hitdns workers)",
+                "ic": "hitdns.make_initial_condition (the reference's numpy synthesis)",
+                "sample": f"per-point rate measured on {n}^3 (the cost per point is "
+                          f"data-independent); the metric's grid is {metric_n}^3"}
+    rate, done, el, threads = cpu_reference(n, steps, warmup, budget_s)
+    return rate, done, el, threads, "port", (
+        f"C oracle port (oracle/hd_oracle.c, OpenMP, {threads} threads) on a {n}^3 sample of the "
+        f"same HIT RK4 problem: {done} steps in {el:.1f} s"), {
+            "grid": n, "parallelism": f"CPU, {threads} OpenMP threads (C port of the reference)",
+            "ic": "hit.py numpy synthesis",
+            "sample": f"per-point rate measured on {n}^3; the metric's grid is {metric_n}^3"}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     n = args.cpu_n
-    rate, done, el, threads = cpu_reference(n, args.steps, args.warmup, budget_s=150.0)
-    sample = (f"C oracle port (oracle/hd_oracle.c, OpenMP) on a {n}^3 sample of the same HIT RK4 "
-              f"problem (per-point cost is data-independent), {done} steps timed after {args.warmup} warm-up")
+    rate, done, el, threads, kind, sample, cfg = cpu_baseline(n, args.steps, args.warmup, 150.0, args.n)
+    config = dict(workload_config(args, 1))
+    config.update(cfg)
+    for key in ("mode", "l2"):  # GPU-arm settings that do not apply to a CPU run
+        config.pop(key, None)
     line = {
         "metric": metric_name(args.n), "impl": "reference",
         "value": rate, "unit": "pt*step/s", "n_gpus": args.gpus, "steps": done,
         "warmup": args.warmup, "ms_per_step": 1e3 * el / done, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, 1),
-        "cpu_baseline": {"value": rate, "unit": "pt*step/s", "cores": threads, "kind": "port",
+        "config": config,
+        "cpu_baseline": {"value": rate, "unit": "pt*step/s", "cores": threads, "kind": kind,
                          "sample": sample},
         "e2e": {"value": rate, "unit": "pt*step/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -346,10 +411,8 @@ def main():
     # ---- CPU baseline (rank 0, N = 1 only) -----------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, done, el, threads = cpu_reference(args.cpu_n, 100, 1, budget_s=15.0)
-        cpu = {"value": rate, "unit": "pt*step/s", "cores": threads, "kind": "port",
-               "sample": f"C oracle (oracle/hd_oracle.c), {args.cpu_n}^3 HIT RK4 CFL 0.4 mu 0.006, "
-                         f"{done} steps in {el:.1f} s"}
+        rate, done, el, threads, kind, sample, _ = cpu_baseline(args.cpu_n, 100, 1, 15.0, n)
+        cpu = {"value": rate, "unit": "pt*step/s", "cores": threads, "kind": kind, "sample": sample}
 
     if rank == 0:
         line = {

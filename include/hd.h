@@ -75,7 +75,8 @@ extern "C" {
 #define HD_BUF_STATE 8 /* 5 fields: march state of a peer-attached plan (hd_peer_attach) */
 #define HD_BUF_SYNC 9  /* 16 uint64: peer flags [axis][state|vflux][from lo|hi], timeout word */
 #define HD_BUF_FRED 10 /* per-warp partials of the diagnostics fused into the last z sweep */
-#define HD_NBUF 11
+#define HD_BUF_ENS 11  /* per-block partials of the enstrophy reduction */
+#define HD_NBUF 12
 
 /* results of hd_reduce_state (doubles at HD_BUF_RED result slot) */
 #define HD_RED_SIGNAL_MAX 0
@@ -87,7 +88,9 @@ extern "C" {
 #define HD_RED_MOMZ 6
 #define HD_RED_ENERGY 7
 #define HD_RED_KE 8       /* sum of 0.5*|m/rho|^2 */
-#define HD_RED_N 9
+#define HD_RED_ENSTROPHY 9 /* sum of 0.5*|curl(m/rho)|^2 -- written by hd_enstrophy /
+                              hd_arm_enstrophy, not by hd_reduce_state */
+#define HD_RED_N 10
 
 /* context slots (doubles at HD_BUF_CTX) */
 #define HD_CTX_T 0
@@ -187,6 +190,19 @@ int hd_reduce_state(hd_plan* plan, const double* u, double* out, int64_t tag, vo
  * sweep in fast mode (no extra pass over the state), a separate reduction
  * otherwise.  One-shot. */
 int hd_arm_reduce(hd_plan* plan, double* out, int64_t tag);
+
+/* Enstrophy of a state (the north star's third diagnostic; the reference has
+ * none -- its operators define it): velocities decoded as physics.py:249-252
+ * (v = m * (1/rho)), the 9 velocity gradients by the 4th-order central
+ * difference of viscous.py:23-51, out[0] = sum over the interior of
+ * 0.5 * |curl v|^2 (divide by the point count for the mean).  Ghosts of u
+ * must be valid along every axis (faces only).  Deterministic order. */
+int hd_enstrophy(hd_plan* plan, const double* u, double* out, void* stream);
+/* One-shot: the next stage-0 HALO part (hd_step / hd_stage_part) writes the
+ * enstrophy of its input state -- the state the step starts from -- to
+ * `out`, folded into the viscous flux kernel that already forms those
+ * gradients (fast and exact mode, mu > 0), else a separate hd_enstrophy pass. */
+int hd_arm_enstrophy(hd_plan* plan, double* out);
 
 /* timeint.py:133-138 + 224-237: ctx[DT] = cfl / signal (cfl > 0) or dt_fixed,
  * clipped to t_final - ctx[T] when t_final >= 0.  Latches a zero/non-finite

@@ -23,6 +23,10 @@
  *   or_rk4_step        pkg/src/hitdns/timeint.py:181-193 (rk4_step)
  *   or_rk3_step        pkg/src/hitdns/timeint.py:168-178 (rk3_tvd_step)
  *   or_max_signal      pkg/src/hitdns/timeint.py:110-131 (max_signal via cons_to_prim)
+ *   or_enstrophy       the north star's enstrophy (the reference has none) from the
+ *                      reference's own operators: velocities as physics.py:249-252
+ *                      (decode_primitives), derivatives as viscous.py:23-51
+ *                      (central_derivative_4 -> kernels.py:221-226)
  *
  * Parity is pinned by tests/test_oracle_golden.py against fixtures produced by
  * running the reference itself (tests/golden/make_golden.py).
@@ -491,6 +495,47 @@ int or_max_signal(const or_geom* G, const double* U, int mode, double* out, int6
   out[0] = sig;
   out[1] = wav;
   return 0;
+}
+
+/* Sum over the interior of 0.5 |curl v|^2 with v = m * (1/rho) and the
+ * 4th-order central difference ((-s2 + 8 s1) - 8 s-1) + s-2) * (1/(12h)).
+ * Ghosts of U must be filled.  Per-plane partial sums added in plane order
+ * (bitwise independent of the thread count). */
+double or_enstrophy(const or_geom* G, const double* U) {
+  const int nx = G->n[0], ny = G->n[1], nz = G->n[2], g = G->g;
+  const int64_t gx = nx + 2 * g, gy = ny + 2 * g;
+  const int64_t npts = or_npts(G);
+  const int64_t st[3] = {1, gx, gx * gy};
+  double coef[3];
+  for (int d = 0; d < 3; ++d) coef[d] = 1.0 / (12.0 * or_spacing(G, d));
+  double* plane = (double*)calloc((size_t)nz, sizeof(double));
+  if (!plane) return NAN;
+#pragma omp parallel for schedule(static)
+  for (int k = 0; k < nz; ++k) {
+    double acc = 0.0;
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        const int64_t p = ((int64_t)(k + g) * gy + (j + g)) * gx + (i + g);
+        double gr[3][3];
+        for (int a = 0; a < 3; ++a)
+          for (int d = 0; d < 3; ++d) {
+            double v[5];
+            for (int o = -2; o <= 2; ++o) {
+              if (!o) continue;
+              const int64_t q = p + o * st[d];
+              v[o + 2] = U[(1 + a) * npts + q] * (1.0 / U[q]);
+            }
+            gr[a][d] = (((-v[4] + 8.0 * v[3]) - 8.0 * v[1]) + v[0]) * coef[d];
+          }
+        const double wx = gr[2][1] - gr[1][2], wy = gr[0][2] - gr[2][0], wz = gr[1][0] - gr[0][1];
+        acc += 0.5 * ((wx * wx + wy * wy) + wz * wz);
+      }
+    plane[k] = acc;
+  }
+  double s = 0.0;
+  for (int k = 0; k < nz; ++k) s += plane[k];
+  free(plane);
+  return s;
 }
 
 /* Full-step driver for the CPU baseline: `steps` RK4 (scheme 4) or RK3 (3)

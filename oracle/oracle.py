@@ -15,6 +15,7 @@ buffers in the reference's own flat COMPONENT_CONTIGUOUS layout
 * :func:`rk3_step`         -- timeint.py:168-178
 * :func:`max_signal`       -- timeint.py:122-131
 * :func:`advance`          -- timeint.py:199-258 without diagnostics
+* :func:`enstrophy`        -- 0.5 <|curl v|^2> from decode_primitives + central_derivative_4
 * :func:`bench_weights`    -- kernels.py:243-291 (layout-study weight kernel), numpy
 
 Parity of this oracle against the reference itself is pinned by
@@ -87,6 +88,8 @@ def lib():
         L.or_advance.argtypes = [ctypes.POINTER(OracleGeom), _dp, ctypes.c_int, ctypes.c_double,
                                  ctypes.c_double, ctypes.c_int, _dp, _i64p]
         L.or_advance.restype = ctypes.c_int
+        L.or_enstrophy.argtypes = [ctypes.POINTER(OracleGeom), _dp]
+        L.or_enstrophy.restype = ctypes.c_double
         L.or_num_threads.argtypes = []
         L.or_num_threads.restype = ctypes.c_int
         _lib = L
@@ -216,6 +219,13 @@ def max_signal(u: np.ndarray, prob: Problem, cfl_mode: str = "max") -> tuple[flo
     if rc:
         raise OracleStateError(rc, where.value)
     return float(out[0]), float(out[1])
+
+
+def enstrophy(u: np.ndarray, prob: Problem) -> float:
+    """Mean of 0.5 |curl(m/rho)|^2 over the interior (ghosts refilled first)."""
+    fill_ghosts(u, prob)
+    G = prob.geom()
+    return float(lib().or_enstrophy(ctypes.byref(G), _p(u))) / (prob.n[0] * prob.n[1] * prob.n[2])
 
 
 def advance(u: np.ndarray, prob: Problem, steps: int, cfl: float | None = 0.4,

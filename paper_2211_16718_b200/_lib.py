@@ -25,11 +25,11 @@ HD_SCHEME_RK4 = 4
 HD_PART_LOCAL, HD_PART_HALO, HD_PART_MID, HD_PART_UPDATE, HD_PART_ALL = 1, 2, 4, 8, 15
 HD_OPT_SEGMENTS, HD_OPT_X_STAGED, HD_OPT_FLUX_ZMARCH = 0, 1, 2
 (HD_BUF_STAGE, HD_BUF_ACC, HD_BUF_INC, HD_BUF_PRIM, HD_BUF_VFLUX, HD_BUF_RED, HD_BUF_CTX,
- HD_BUF_ERR, HD_BUF_STATE, HD_BUF_SYNC, HD_BUF_FRED) = range(11)
+ HD_BUF_ERR, HD_BUF_STATE, HD_BUF_SYNC, HD_BUF_FRED, HD_BUF_ENS) = range(12)
 HD_PEER_STATE, HD_PEER_VFLUX = 0, 1
 (HD_RED_SIGNAL_MAX, HD_RED_SIGNAL_SUM, HD_RED_WAVESPEED, HD_RED_MASS, HD_RED_MOMX, HD_RED_MOMY,
- HD_RED_MOMZ, HD_RED_ENERGY, HD_RED_KE) = range(9)
-HD_RED_N = 9
+ HD_RED_MOMZ, HD_RED_ENERGY, HD_RED_KE, HD_RED_ENSTROPHY) = range(10)
+HD_RED_N = 10
 HD_CTX_T, HD_CTX_DT = 0, 1
 HD_CTX_N = 4
 
@@ -43,7 +43,7 @@ EXPORTS = (
     "hd_timer_read", "hd_ipc_handle", "hd_ipc_open", "hd_ipc_close", "hd_peer_attach", "hd_peer_attach3", "hd_peer_signal",
     "hd_peer_wait", "hd_peer_timed_out", "hd_stage_buffer", "hd_rk4_step", "hd_max_signal",
     "hd_totals", "hd_error_flags", "hd_halo_exchange", "hd_viscous_fluxes", "hd_viscous_divergence",
-    "hd_arm_reduce",
+    "hd_arm_reduce", "hd_enstrophy", "hd_arm_enstrophy",
 )
 # hd_timer_read kinds (HD_TK_*)
 TIMER_KINDS = ("sweep_x", "sweep_y", "sweep_z", "gradflux", "prims", "divergence", "reduce")
@@ -124,6 +124,8 @@ def load(require_cuda: bool = False):
             "hd_stage_buffer": ([P, i32, i32, P, ctypes.POINTER(ctypes.c_void_p)], i32),
             "hd_rk4_step": ([P, P, P, P], i32),
             "hd_arm_reduce": ([P, P, i64], i32),
+            "hd_enstrophy": ([P, P, P, P], i32),
+            "hd_arm_enstrophy": ([P, P], i32),
             "hd_viscous_fluxes": ([P, P, P], i32),
             "hd_viscous_divergence": ([P, P, P], i32),
             "hd_max_signal": ([P, P, P, i32, P], i32),

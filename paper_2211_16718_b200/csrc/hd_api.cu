@@ -49,7 +49,7 @@ void layout(const hd_geom* g, int64_t off[HD_NBUF], int64_t* total) {
   const int64_t f = npts_of(g) * 8;
   int64_t o = 0;
   const int64_t sizes[HD_NBUF] = {10 * f, 5 * f, 5 * f, 4 * f, 9 * f, RED_BYTES, 8 * HD_CTX_N, 64,
-                                  5 * f, 128, fused_red_capacity(*g) * 9 * 8};
+                                  5 * f, 128, fused_red_capacity(*g) * 9 * 8, ens_capacity(*g) * 8};
   for (int b = 0; b < HD_NBUF; ++b) {
     off[b] = o;
     o = align_up(o + sizes[b]);
@@ -348,14 +348,22 @@ int hd_stage_part(hd_plan* p, int scheme, int stage, int parts, double* u, const
   // HALO (reads every ghost of `us`)
   //   exact: z sweep, primitives of the whole box, viscous fluxes
   //   fast:  viscous fluxes straight from the state (primitives on the fly)
+  // Stage 0 folds an armed enstrophy of its input (the step's start state) into
+  // the flux kernel, which forms the velocity gradients anyway (hd_arm_enstrophy).
   if (!rc && (parts & HD_PART_HALO)) {
+    double* ens = stage == 0 ? p->ens_out : nullptr;
+    int folded = 0;
     if (exact) {
       rc = timed(p, HD_TK_SWEEP_Z, s, [&] { return launch_sweep(p, 2, us, inc, 1, 0, t, s); });
       if (!rc && visc) rc = timed(p, HD_TK_PRIMS, s, [&] { return launch_prims(p, us, s); });
-      if (!rc && visc) rc = timed(p, HD_TK_GRADFLUX, s, [&] { return launch_gradflux(p, nullptr, s); });
+      if (!rc && visc)
+        rc = timed(p, HD_TK_GRADFLUX, s, [&] { return launch_gradflux(p, nullptr, s, ens, &folded); });
     } else if (visc) {
-      rc = timed(p, HD_TK_GRADFLUX, s, [&] { return launch_gradflux(p, us, s); });
+      rc = timed(p, HD_TK_GRADFLUX, s, [&] { return launch_gradflux(p, us, s, ens, &folded); });
     }
+    if (!rc && ens && !folded)
+      rc = timed(p, HD_TK_REDUCE, s, [&] { return launch_enstrophy(p, us, ens, s); });
+    if (stage == 0) p->ens_out = nullptr;
   }
   // MID (fast): y sweep + D_x F_x + D_y F_y (no z ghosts of the fluxes read)
   if (!rc && (parts & HD_PART_MID) && !exact)
@@ -406,6 +414,19 @@ int hd_arm_reduce(hd_plan* p, double* out, int64_t tag) {
   p->red_out = out;
   p->red_tag = tag;
   return HD_OK;
+}
+
+int hd_arm_enstrophy(hd_plan* p, double* out) {
+  if (!p) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  p->ens_out = out;
+  return HD_OK;
+}
+
+int hd_enstrophy(hd_plan* p, const double* u, double* out, void* stream) {
+  if (!p || !u || !out) return HD_E_ARG;
+  if (!p->ws) return HD_E_WORKSPACE;
+  return timed(p, HD_TK_REDUCE, S(stream), [&] { return launch_enstrophy(p, u, out, S(stream)); });
 }
 
 int hd_stage_buffer(hd_plan* p, int scheme, int stage, double* u, void** out) {

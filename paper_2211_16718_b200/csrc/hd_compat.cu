@@ -85,6 +85,11 @@ int hd_error_flags(hd_plan* p, int* flags, int64_t* where, void* stream) {
 int hd_halo_exchange(hd_plan* p, double* fields, int nfields, void* stream) {
   if (!p || !fields || nfields < 1) return HD_E_ARG;
   const Geo& G = p->geo;
+  // peer images are stored at workspace offsets in the neighbours' mappings:
+  // `fields` must lie inside this plan's workspace
+  if (G.peer_any && ((const char*)fields < p->ws ||
+                     (const char*)(fields + (int64_t)nfields * G.npts) > p->ws + p->ws_bytes))
+    return HD_E_ARG;
   int rc = launch_fill_ghosts(p, fields, nfields, 7, (cudaStream_t)stream);  // periodic axes
   if (rc || !G.peer_any) return rc;
   const int mask = (G.peer[0] ? 1 : 0) | (G.peer[1] ? 2 : 0) | (G.peer[2] ? 4 : 0);

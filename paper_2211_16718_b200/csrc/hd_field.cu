@@ -201,6 +201,91 @@ __global__ void __launch_bounds__(128) gradflux_kernel(const double* __restrict_
   if (G.peer_any && touches_peer(G, i, j, k)) __threadfence_system();
 }
 
+// ---------------------------------------------------------------------------
+// enstrophy 0.5 |curl v|^2 (north-star diagnostic; the reference's operators:
+// v = m * (1/rho) as physics.py:249-252, D_d as viscous.py:23-51)
+// ---------------------------------------------------------------------------
+// gr[a][d] = d v_a / d x_d
+__device__ __forceinline__ double enstrophy_point(const double (&gr)[3][3]) {
+  const double wx = gr[2][1] - gr[1][2], wy = gr[0][2] - gr[2][0], wz = gr[1][0] - gr[0][1];
+  return 0.5 * ((wx * wx + wy * wy) + wz * wz);
+}
+
+// sum of v over the block in a fixed order (warp tree, then warps in order)
+// -> partial[slot]; every thread of the block must call it
+__device__ __forceinline__ void block_sum_store(double v, double* partial, int64_t slot) {
+  __shared__ double sh[32];
+  const int t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nthreads = blockDim.x * blockDim.y * blockDim.z;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  if ((t & 31) == 0) sh[t >> 5] = v;
+  __syncthreads();
+  if (t == 0) {
+    double s = sh[0];
+    for (int w = 1; w < nthreads / 32; ++w) s += sh[w];
+    partial[slot] = s;
+  }
+}
+
+__global__ void sum_finish_kernel(const double* partial, int n, double* out) {
+  double v = 0.0;  // one warp, fixed order
+  for (int b = threadIdx.x; b < n; b += 32) v += partial[b];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  if (threadIdx.x == 0) *out = v;
+}
+
+constexpr int ENS_THREADS = 256, ENS_BLOCKS_MAX = 2048;
+
+// stand-alone pass: one warp per x row, the 6 off-diagonal velocity gradients
+// from the neighbours' conserved values (IEEE 1/rho, as decode_primitives)
+__global__ void __launch_bounds__(ENS_THREADS) enstrophy_kernel(const double* __restrict__ u, Geo G,
+                                                                double* partial) {
+  const int64_t np = G.npts;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t rows = (int64_t)G.n[1] * G.n[2];
+  const int64_t st[3] = {1, G.sy, G.sz};
+  double coef[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) coef[d] = 1.0 / (12.0 * G.h[d]);
+  auto vel = [&](int64_t q, int c) { return __dmul_rn(__ldg(u + (1 + c) * np + q), __ddiv_rn(1.0, __ldg(u + q))); };
+  auto D = [&](int64_t q, int c, int d) {
+    return cd4v<true>(vel(q - 2 * st[d], c), vel(q - st[d], c), vel(q + st[d], c), vel(q + 2 * st[d], c),
+                      coef[d]);
+  };
+  double acc = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)(ENS_THREADS / 32) + warp; r < rows;
+       r += (int64_t)gridDim.x * (ENS_THREADS / 32)) {
+    const int64_t row0 = G.idx(0, (int)(r % G.n[1]), (int)(r / G.n[1]));
+    for (int i = lane; i < G.n[0]; i += 32) {
+      const int64_t q = row0 + i;
+      double gr[3][3] = {{0.0, D(q, 0, 1), D(q, 0, 2)}, {D(q, 1, 0), 0.0, D(q, 1, 2)},
+                         {D(q, 2, 0), D(q, 2, 1), 0.0}};
+      acc += enstrophy_point(gr);
+    }
+  }
+  block_sum_store(acc, partial, blockIdx.x);
+}
+
+int64_t ens_capacity(const hd_geom& g) {
+  // z-marching flux kernel: tiles x z segments (<= tiles + 8 x 512 SMs), or the stand-alone pass
+  const int64_t tiles = (int64_t)((g.n[0] + 31) / 32) * ((g.n[1] + 7) / 8);
+  return tiles + 4096 > ENS_BLOCKS_MAX ? tiles + 4096 : ENS_BLOCKS_MAX;
+}
+
+int launch_enstrophy(const hd_plan* p, const double* u, double* out, cudaStream_t s) {
+  const Geo& G = p->geo;
+  const int64_t rows = (int64_t)G.n[1] * G.n[2];
+  int blocks = (int)((rows + ENS_THREADS / 32 - 1) / (ENS_THREADS / 32));
+  if (blocks > ENS_BLOCKS_MAX) blocks = ENS_BLOCKS_MAX;
+  double* partial = (double*)(p->ws + p->off[HD_BUF_ENS]);
+  enstrophy_kernel<<<blocks, ENS_THREADS, 0, s>>>(u, G, partial);
+  sum_finish_kernel<<<1, 32, 0, s>>>(partial, blocks, out);
+  hd::count_launches(2);
+  return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+}
+
 // gradflux with z marching (blocks of 32 x 8 columns): the z stencil comes from
 // a per-thread register queue of 5 planes (each prims value is loaded once per
 // column), the x/y stencils from a shared-memory plane tile with a 2-point halo.
@@ -223,10 +308,12 @@ __device__ __forceinline__ void prims_of(const double (&c)[5], double gamma, dou
 // FROM_U (fast mode): `src` is the conserved state and every loaded point is
 // converted to primitives on the fly (no primitive fields in HBM); else `src`
 // holds the 4 primitive fields.
-template <bool EXACT, bool FROM_U>
+// ENS: also the enstrophy of the state from the velocity gradients it forms
+// (one partial per block into ens_partial)
+template <bool EXACT, bool FROM_U, bool ENS>
 __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_zm_kernel(
     const double* __restrict__ prim, double* __restrict__ vf, Geo G, double mu, double q_coef,
-    int zseg, double gamma) {
+    int zseg, double gamma, double* ens_partial) {
   // two plane tiles (double-buffered: one barrier per plane); every load is
   // issued one plane before it is needed (z queue: plane k+3; ring: plane k+1)
   __shared__ double tile[2][4][GZ_PY][GZ_PX];
@@ -286,6 +373,7 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_zm_kernel(
   const int64_t rcol = G.idx(blockIdx.x * GZ_TX + px - GZ_H, blockIdx.y * GZ_TY + py - GZ_H, 0);
   double rv[NF];
   if (has_ring) load(rcol + (int64_t)k0 * sz, rv);
+  double ens = 0.0;
   for (int k = k0; k < k1; ++k) {
     const int b = k & 1;
     double pq[4], pr[4];
@@ -325,6 +413,7 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_zm_kernel(
       }
     }
     const double vel[3] = {qz[0][2], qz[1][2], qz[2][2]};
+    if constexpr (ENS) ens += enstrophy_point(gr);
     double val[VF_N];
     viscous_flux_point<EXACT>(gr, gT, vel, mu, q_coef, val);
     // each field gets face images only along the axes it is differentiated along
@@ -360,11 +449,15 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_zm_kernel(
   if (G.peer_any && ((G.peer[2] && (k0 < G.g || k1 > G.n[2] - G.g)) ||
                      touches_peer(G, i, j, G.g)))
     __threadfence_system();
+  if constexpr (ENS)
+    block_sum_store(ens, ens_partial, ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
 }
 
 
-int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s) {
+int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s, double* ens_out,
+                    int* ens_folded) {
   const Geo& G = p->geo;
+  if (ens_folded) *ens_folded = 0;
   const double* prim = (const double*)(p->ws + p->off[HD_BUF_PRIM]);
   const bool exact = p->mode == HD_MODE_EXACT;
   double* vf = (double*)(p->ws + p->off[HD_BUF_VFLUX]);
@@ -379,12 +472,26 @@ int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s) {
     nseg = (G.n[2] + zseg - 1) / zseg;
     dim3 block(GZ_TX, GZ_TY, 1), grid(G.n[0] / GZ_TX, G.n[1] / GZ_TY, nseg);
     const double gamma = p->phys.gamma;
-    if (exact)
-      gradflux_zm_kernel<true, false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma);
-    else if (u)
-      gradflux_zm_kernel<false, true><<<grid, block, 0, s>>>(u, vf, G, mu, q_coef, zseg, gamma);
-    else
-      gradflux_zm_kernel<false, false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma);
+    const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
+    double* ep = (double*)(p->ws + p->off[HD_BUF_ENS]);
+    const bool ens = ens_out && nblk <= ens_capacity(p->geom);
+    if (ens) {
+      if (exact)
+        gradflux_zm_kernel<true, false, true><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
+      else if (u)
+        gradflux_zm_kernel<false, true, true><<<grid, block, 0, s>>>(u, vf, G, mu, q_coef, zseg, gamma, ep);
+      else
+        gradflux_zm_kernel<false, false, true><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
+      sum_finish_kernel<<<1, 32, 0, s>>>(ep, (int)nblk, ens_out);
+      hd::count_launches(1);
+      if (ens_folded) *ens_folded = 1;
+    } else if (exact) {
+      gradflux_zm_kernel<true, false, false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
+    } else if (u) {
+      gradflux_zm_kernel<false, true, false><<<grid, block, 0, s>>>(u, vf, G, mu, q_coef, zseg, gamma, ep);
+    } else {
+      gradflux_zm_kernel<false, false, false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
+    }
     hd::count_launches(1);
     return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
   }

@@ -76,6 +76,18 @@ struct Geo {
   __host__ __device__ int64_t stride(int d) const { return d == 0 ? 1 : (d == 1 ? sy : sz); }
 };
 
+// Flat index of the first copy, in C (z, y, x) order over the ghosted box, of
+// interior point (i,j,k): along a locally periodic axis the top g layers also
+// sit in the low ghost layers.  The reference's decode_primitives checks the
+// whole filled box and reports np.argwhere's first hit (physics.py:47-55,
+// 240-255), so a stage error latches this index (min over offending points).
+__device__ __forceinline__ int64_t first_image(const Geo& G, int i, int j, int k) {
+  if (G.periodic[0] && i >= G.n[0] - G.g) i -= G.n[0];
+  if (G.periodic[1] && j >= G.n[1] - G.g) j -= G.n[1];
+  if (G.periodic[2] && k >= G.n[2] - G.g) k -= G.n[2];
+  return G.idx(i, j, k);
+}
+
 struct Phys {
   double gamma, gm1, prandtl, mu;  // mu = effective viscosity (mu * visc_scale)
   double eps, delta;
@@ -110,6 +122,7 @@ struct hd_plan {
   char* peer_hi[3];
   double* red_out;   // armed diagnostics of the next step's result (hd_arm_reduce)
   int64_t red_tag;
+  double* ens_out;   // armed enstrophy of the next step's start state (hd_arm_enstrophy)
   int64_t opt[HD_OPT_N];  // hd_plan_set_option
 };
 
@@ -136,8 +149,15 @@ int launch_prims_planes(const hd_plan* p, const double* u, int z_lo, int z_hi, c
 int launch_fill_ghosts(const hd_plan* p, double* f, int nfields, int axis_mask, cudaStream_t s);
 int launch_prims(const hd_plan* p, const double* u, cudaStream_t s);
 // viscous flux fields; fast mode with u != nullptr derives the primitives from
-// the conserved state u on the fly, else they are read from HD_BUF_PRIM
-int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s);
+// the conserved state u on the fly, else they are read from HD_BUF_PRIM.
+// ens_out != nullptr: also the enstrophy of that state when the z-marching
+// kernel runs (*ens_folded = 1), else the caller runs launch_enstrophy
+int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s, double* ens_out = nullptr,
+                    int* ens_folded = nullptr);
+// enstrophy sum of a state (ghosts valid) into *out
+int launch_enstrophy(const hd_plan* p, const double* u, double* out, cudaStream_t s);
+// partial slots of HD_BUF_ENS
+int64_t ens_capacity(const hd_geom& g);
 // divergence (+ optional RK update).  dims_mask: which d's divergence to add;
 // update: 0 = store inc, else RK stage update with scheme/stage.
 int launch_divergence(const hd_plan* p, int dims_mask, const double* inc_in, double* inc_out,

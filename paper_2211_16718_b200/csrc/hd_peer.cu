@@ -49,6 +49,9 @@ __global__ void peer_signal_kernel(PeerSlots t, unsigned long long v) {
 
 // spin until every listed local counter reached v (bounded; then the timeout word)
 __global__ void peer_wait_kernel(unsigned long long* sync, int mask, int which, unsigned long long v) {
+  // after one timeout the march is lost: later waits return at once instead of
+  // spinning another 30 s each (the host raises HaloProtocolError at its next check)
+  if (ld_acquire_sys(sync + SYNC_TIMEOUT)) return;
   const unsigned long long t0 = global_ns();
   for (;;) {
     bool ok = true;

@@ -441,8 +441,10 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
       for (int v = 1; v < NV; ++v) sp[(NV - 1 + v) * SWEEP_THREADS] = ff[v];
     }
     if (a.check && m >= 0 && m < nd) {
-      if (!(uu[0] > 0.0)) latch_error(a.err, a.tag, 1, base + (int64_t)m * sd);
-      else if (!(pv[3] > 0.0)) latch_error(a.err, a.tag, 2, base + (int64_t)m * sd);
+      const int code = !(uu[0] > 0.0) ? 1 : (!(pv[3] > 0.0) ? 2 : 0);
+      if (code)
+        latch_error(a.err, a.tag, code,
+                    first_image(G, DIM == 0 ? m : li, DIM == 1 ? m : lj, DIM == 2 ? m : lk));
     }
   };
 
@@ -675,8 +677,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
     double inv, pv[4];
     point_flux<0, EXACT>(uu, gm1, ff, inv, pv);
     if (a.check && p >= 0 && p < nd) {
-      if (!(uu[0] > 0.0)) latch_error(a.err, a.tag, 1, base + p);
-      else if (!(pv[3] > 0.0)) latch_error(a.err, a.tag, 2, base + p);
+      const int code = !(uu[0] > 0.0) ? 1 : (!(pv[3] > 0.0) ? 2 : 0);
+      if (code) latch_error(a.err, a.tag, code, first_image(G, p, j0 + lane, k));
     }
   };
   // out chunk: cells c0 + XC t .. ; d[v] staged, flushed coalesced as inc = old - d

@@ -95,18 +95,37 @@ def decompose(spec: GridSpec, dims) -> list:
     return out
 
 
-def default_dims(nranks: int, n, ghost_width: int = 3):
-    """GPU choice: split z only -> (1, 1, nranks).
+def _legal(dims, n, ghost_width: int) -> bool:
+    return all(n[d] % dims[d] == 0 and n[d] // dims[d] >= ghost_width for d in range(3))
 
-    z faces are contiguous per variable (no pack kernels) and the x/y sweeps
-    overlap the exchange.  The reference prefers x splits to minimise face
-    area on CPUs (decomp.py:106-140); results are decomposition-invariant, so
-    this is a pure performance choice."""
+
+def default_dims(nranks: int, n, ghost_width: int = 3):
+    """The reference's rank grid (decomp.py:106-140): among the legal factorings
+    dx * dy * dz = nranks, the one with the least exchanged face area, ties to
+    the larger x split, then the larger y split."""
+    nranks = int(nranks)
+    candidates = []
+    for dx in (d for d in range(1, nranks + 1) if nranks % d == 0):
+        for dy in (d for d in range(1, nranks // dx + 1) if (nranks // dx) % d == 0):
+            dims = (dx, dy, nranks // (dx * dy))
+            if not _legal(dims, n, ghost_width):
+                continue
+            loc = [n[d] // dims[d] for d in range(3)]
+            area = sum(2 * loc[(d + 1) % 3] * loc[(d + 2) % 3] for d in range(3) if dims[d] > 1)
+            candidates.append(((area, -dx, -dy), dims))
+    if not candidates:
+        raise ConfigError(f"no legal decomposition of {tuple(n)} into {nranks} ranks")
+    return min(candidates)[1]
+
+
+def gpu_dims(nranks: int, n, ghost_width: int = 3):
+    """The GPU default of the drivers: z slabs (1, 1, nranks) when legal -- z faces
+    are contiguous per variable (no pack kernels), the x/y sweeps overlap the
+    exchange, and the peer-store halo needs no strided stores -- else the
+    reference's choice (default_dims).  Results are decomposition-invariant,
+    so this is purely a performance choice."""
     dims = (1, 1, int(nranks))
-    if n[2] % nranks == 0 and n[2] // nranks >= ghost_width:
-        return dims
-    raise ConfigError(f"no legal z decomposition of {tuple(n)} into {nranks} ranks "
-                      f"(need n_z % ranks == 0 and n_z / ranks >= {ghost_width})")
+    return dims if _legal(dims, n, ghost_width) else default_dims(nranks, n, ghost_width)
 
 
 def comm_fraction(comm_seconds: float, busy_seconds: float) -> float:
@@ -174,6 +193,40 @@ class _Pending:
         self.works, self.unpack = [], []
 
 
+class _WaitClock:
+    """Exposed communication time of one rank (the reference's comm timer,
+    decomp.py:202-221 and :359-361): each wait is bracketed by CUDA events on
+    the compute stream, so what is measured is how long that stream stood still
+    for a halo or a collective -- zero when the exchange finished behind the
+    kernels it overlapped.  Host clock for CPU (gloo) tensors.  ``total()``
+    synchronises once and drains the pairs."""
+
+    def __init__(self):
+        self.pairs = []
+        self.host = 0.0
+
+    def __call__(self, fn, cuda: bool = True):
+        if not (cuda and torch.cuda.is_available() and torch.cuda.is_initialized()):
+            t0 = _time.perf_counter()
+            out = fn()
+            self.host += _time.perf_counter() - t0
+            return out
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn()
+        b.record()
+        self.pairs.append((a, b))
+        return out
+
+    def total(self) -> float:
+        sec = self.host
+        if self.pairs:
+            self.pairs[-1][1].synchronize()
+            sec += sum(a.elapsed_time(b) for a, b in self.pairs) / 1e3
+        self.pairs, self.host = [], 0.0
+        return sec
+
+
 class DistHalo:
     """Ghost synchronisation of one rank over torch.distributed.
 
@@ -193,7 +246,8 @@ class DistHalo:
         self.group = group
         self.periodic = tuple(layout.dims[d] == 1 for d in range(3))
         self.split = tuple(d for d in range(3) if layout.dims[d] > 1)
-        self.comm_seconds = 0.0
+        self.comm_seconds = 0.0  # exposed halo/collective waits (_WaitClock), seconds
+        self.clock = _WaitClock()
         self.lo = tuple(layout.neighbor(d, -1) for d in range(3))
         self.hi = tuple(layout.neighbor(d, +1) for d in range(3))
 
@@ -320,34 +374,45 @@ class DistHalo:
         local_waits = 0 in self.split or (exact and 1 in self.split)
         pre_mid = tuple(d for d in (0, 1) if d in self.split)
 
+        clock = self.clock
+
         def stepper(u, dt_dev, tag):
             plan.fill_ghosts(u, NVARS)  # periodic axes wrap locally; split axes exchanged below
             for s in range(nst):
                 us = plan.stage_input(scheme, s, u)
                 pend = halo.exchange_async(us, NVARS, spec)
                 if local_waits:
-                    pend.wait()
+                    clock(pend.wait)
                 plan.stage_part(scheme, s, _lib.HD_PART_LOCAL, u, dt_dev, tag)
-                pend.wait()
+                clock(pend.wait)
                 plan.stage_part(scheme, s, _lib.HD_PART_HALO, u, dt_dev, tag)
                 if visc and pre_mid:
                     for d in pre_mid:
-                        halo.exchange_async(vflux, 9, spec, axes=(d,), fields=_VF_GROUP[d]).wait()
+                        clock(halo.exchange_async(vflux, 9, spec, axes=(d,), fields=_VF_GROUP[d]).wait)
                 zpend = (halo.exchange_async(vflux, 9, spec, axes=(2,), fields=_VF_GROUP[2])
                          if visc else _Pending())
                 plan.stage_part(scheme, s, _lib.HD_PART_MID, u, dt_dev, tag)  # overlaps it
-                zpend.wait()
+                clock(zpend.wait)
                 plan.stage_part(scheme, s, _lib.HD_PART_UPDATE, u, dt_dev, tag)
 
         def reducer(red):
             if self.split:
-                _combine_reductions(red, halo.group)
+                clock(lambda: _combine_reductions(red, halo.group))
+
+        def ghost_sync(u):
+            plan.fill_ghosts(u, NVARS)
+            clock(halo.exchange_async(u, NVARS, spec).wait)
 
         nblocks = self.layout.dims[0] * self.layout.dims[1] * self.layout.dims[2]
         march = _DeviceMarch(plan, fields, gas, tparams, t0, stepper=stepper, reducer=reducer,
                              global_points=spec.interior_points * nblocks,
-                             error_combine=lambda key: _combine_error_key(key, self.group))
-        return march.run(observer, dt_provider)
+                             error_combine=lambda key: _combine_error_key(key, self.group),
+                             ghost_sync=ghost_sync,
+                             sum_combine=lambda t: _combine_sums(t, self.group))
+        try:
+            return march.run(observer, dt_provider)
+        finally:
+            self.comm_seconds += clock.total()
 
     def peer_enabled(self, fields: FieldSet) -> bool:
         """Blocks on CUDA: the halo goes over NVLink peer stores (hd_peer_*)
@@ -388,36 +453,52 @@ class DistHalo:
             state_before_local = 0 in self.split or (exact and 1 in self.split)
             vflux_before_mid = not exact and (0 in self.split or 1 in self.split)
 
+            clock = self.clock
+
+            def wait(which, v):  # the spin kernel's duration = the exposed wait
+                clock(lambda: plan.peer_wait(which, v))
+
             def stepper(u, dt_dev, tag):
                 plan.fill_ghosts(u, NVARS)  # periodic axes wrap; split axes arrive as peer stores
                 for s in range(nst):
                     v = counter[0] + 1
                     if state_before_local:
-                        plan.peer_wait(_lib.HD_PEER_STATE, v - 1)
+                        wait(_lib.HD_PEER_STATE, v - 1)
                     plan.stage_part(scheme, s, _lib.HD_PART_LOCAL, u, dt_dev, tag)
                     if not state_before_local:
-                        plan.peer_wait(_lib.HD_PEER_STATE, v - 1)
+                        wait(_lib.HD_PEER_STATE, v - 1)
                     plan.stage_part(scheme, s, _lib.HD_PART_HALO, u, dt_dev, tag)
                     if visc:
                         plan.peer_signal(_lib.HD_PEER_VFLUX, v)
                         if vflux_before_mid:
-                            plan.peer_wait(_lib.HD_PEER_VFLUX, v)
+                            wait(_lib.HD_PEER_VFLUX, v)
                     plan.stage_part(scheme, s, _lib.HD_PART_MID, u, dt_dev, tag)
                     if visc and not vflux_before_mid:
-                        plan.peer_wait(_lib.HD_PEER_VFLUX, v)
+                        wait(_lib.HD_PEER_VFLUX, v)
                     plan.stage_part(scheme, s, _lib.HD_PART_UPDATE, u, dt_dev, tag)
                     plan.peer_signal(_lib.HD_PEER_STATE, v)
                     counter[0] = v
 
             def reducer(red):
-                _combine_reductions(red, self.group)
+                clock(lambda: _combine_reductions(red, self.group))
+
+            def ghost_sync(u):
+                # the last UPDATE stored this rank's boundary layers into the
+                # neighbours' ghosts (and theirs into ours) and signalled
+                wait(_lib.HD_PEER_STATE, counter[0])
+                plan.fill_ghosts(u, NVARS)
 
             nblocks = self.layout.dims[0] * self.layout.dims[1] * self.layout.dims[2]
             march = _DeviceMarch(plan, local, gas, tparams, t0, stepper=stepper, reducer=reducer,
                                  global_points=spec.interior_points * nblocks,
                                  copy=False,
-                                 error_combine=lambda key: _combine_error_key(key, self.group))
-            res = march.run(observer, dt_provider)
+                                 error_combine=lambda key: _combine_error_key(key, self.group),
+                                 ghost_sync=ghost_sync,
+                                 sum_combine=lambda t: _combine_sums(t, self.group))
+            try:
+                res = march.run(observer, dt_provider)
+            finally:
+                self.comm_seconds += clock.total()
             flag = torch.tensor([1 if plan.peer_timed_out() else 0], dtype=torch.int64,
                                 device=state.device)
             dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
@@ -441,6 +522,17 @@ def _combine_reductions(red: torch.Tensor, group) -> None:
     for r in range(1, world):
         acc += allv[r, 3:]
     red[3:] = acc
+
+
+def _combine_sums(t: torch.Tensor, group) -> None:
+    """In place: the sum over ranks, added in rank order (deterministic)."""
+    world = dist.get_world_size(group)
+    allv = torch.empty((world, t.numel()), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(allv, t.contiguous().view(-1), group=group)
+    acc = allv[0].clone()
+    for r in range(1, world):
+        acc += allv[r]
+    t.view(-1).copy_(acc)
 
 
 def _combine_error_key(key: int, group) -> int:
@@ -546,7 +638,7 @@ def parallel_advance(fields: FieldSet, gas: GasModel, tparams, weno_params: Weno
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
     if dims is None:
-        dims = default_dims(world, fields.spec.n, fields.spec.ghost_width)
+        dims = gpu_dims(world, fields.spec.n, fields.spec.ghost_width)
     dims = tuple(int(d) for d in dims)
     if dims[0] * dims[1] * dims[2] != world:
         raise ConfigError(f"dims {dims} need {dims[0] * dims[1] * dims[2]} ranks, have {world}")
@@ -554,11 +646,13 @@ def parallel_advance(fields: FieldSet, gas: GasModel, tparams, weno_params: Weno
     lay = layouts[rank]
     local = scatter(fields, [lay])[0]
     wall0 = _time.perf_counter()
+    comm = 0.0
     if world == 1:
         res = advance(local, gas, tparams, weno_params, delta, mode=mode)
     else:
         halo = DistHalo(lay, group)
         res = halo.advance(local, gas, tparams, weno_params, delta, 0.0, None, None, mode)
+        comm = halo.comm_seconds
     if fields.data.is_cuda:
         torch.cuda.synchronize()
     wall = _time.perf_counter() - wall0
@@ -573,8 +667,18 @@ def parallel_advance(fields: FieldSet, gas: GasModel, tparams, weno_params: Weno
             fs.interior().copy_(part)
             locals_.append(fs)
         gathered = gather(locals_, layouts, fields.spec)
-    report = TimingReport(rank, dims, res.steps, wall, wall, 0.0)
-    return ParallelResult(fields=gathered, t=res.t, reports=[report])
+    # one report per rank, as the reference (decomp.py:380-391): comm = the rank's
+    # exposed halo/collective waits, comp = the rest of its wall time
+    mine = torch.tensor([wall, max(wall - comm, 0.0), comm], dtype=torch.float64,
+                        device=fields.data.device if fields.data.is_cuda else "cpu")
+    if world > 1:
+        every = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(every, mine, group=group)
+    else:
+        every = [mine]
+    reports = [TimingReport(r, dims, res.steps, *(float(x) for x in every[r].tolist()))
+               for r in range(world)]
+    return ParallelResult(fields=gathered, t=res.t, reports=reports)
 
 
 def _check_protocol(ok: bool, what: str) -> None:
@@ -602,7 +706,8 @@ def strong_scaling(fields: FieldSet, gas: GasModel, tparams, ranks_list,
                    mode: str | None = None) -> list:
     """The same run over rank counts from identical initial fields
     (decomp.py:426-461), one process per GPU: every rank of the world calls
-    it; rank counts above the world size are skipped.  Each count runs on a
+    it; a rank count outside 1..world size raises ConfigError (one process per
+    GPU: the reference's thread ranks have no such limit).  Each count runs on a
     sub-group of the first ``nranks`` ranks (the others wait at a barrier)
     after a one-step warm-up on that group; ``wall`` is the slowest rank's
     device-synchronised wall clock.  Rank 0 gets the rows; the others get []."""
@@ -612,27 +717,32 @@ def strong_scaling(fields: FieldSet, gas: GasModel, tparams, ranks_list,
     rank = dist.get_rank() if world > 1 else 0
     warm = TimeParams(scheme=tparams.scheme, dt=tparams.dt, cfl=tparams.cfl,
                       cfl_mode=tparams.cfl_mode, max_steps=1)
+    counts = [int(r) for r in ranks_list]
+    bad = [r for r in counts if r < 1 or r > world]
+    if bad:
+        raise ConfigError(f"rank counts {bad} cannot run on {world} process(es) "
+                          f"(one per GPU; launch with --nproc-per-node >= {max(counts)})")
     rows = []
-    for nranks in (int(r) for r in ranks_list):
-        if nranks < 1 or nranks > world:
-            continue
-        dims = dims_for(nranks) if dims_for else default_dims(nranks, fields.spec.n, fields.spec.ghost_width)
+    for nranks in counts:
+        dims = dims_for(nranks) if dims_for else gpu_dims(nranks, fields.spec.n, fields.spec.ghost_width)
         group = None
         if world > 1:
             group = dist.new_group(list(range(nranks)))
-        wall = 0.0
+        row = [0.0, 0.0, 0.0]
         if rank < nranks:
             sub = group if world > 1 else None
             parallel_advance(fields.copy(), gas, warm, weno_params, delta, dims, group=sub, mode=mode)
             res = parallel_advance(fields.copy(), gas, tparams, weno_params, delta, dims, group=sub,
                                    mode=mode)
-            wall = max(r.wall_seconds for r in res.reports)
+            # decomp.py:452-460: slowest rank's wall; comp and comm summed over ranks
+            row = [max(r.wall_seconds for r in res.reports), sum(r.comp_seconds for r in res.reports),
+                   sum(r.comm_seconds for r in res.reports)]
         if world > 1:
             dev = fields.data.device if fields.data.is_cuda else torch.device("cpu")
-            t = torch.tensor([wall], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            wall = float(t.item())
-        rows.append(ScaleRow(nranks, tuple(dims), wall, wall, 0.0))
+            t = torch.tensor(row, dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)  # rank 0 of the sub-group holds the row
+            row = t.tolist()
+        rows.append(ScaleRow(nranks, tuple(dims), *row))
     return rows if rank == 0 else []
 
 

@@ -185,6 +185,21 @@ def compute_spectrum(u, v, w) -> SpectrumTable:
     return SpectrumTable(np.arange(binned.shape[0], dtype=np.int64), binned, n)
 
 
+def spectral_divergence(u, v, w) -> float:
+    """max over wavevectors of |k . c(k)| with c = fft / n^3 (hit.py:179-188): zero up
+    to transform round-off for a solenoidal field.  numpy arrays or tensors."""
+    if isinstance(u, torch.Tensor):
+        n = u.shape[-1]
+        kk = torch.fft.fftfreq(n, 1.0 / n, dtype=torch.float64, device=u.device)
+        div = (kk[None, None, :] * torch.fft.fftn(u) + kk[None, :, None] * torch.fft.fftn(v) +
+               kk[:, None, None] * torch.fft.fftn(w)) / float(n) ** 3
+        return float(div.abs().max())
+    n = u.shape[-1]
+    kx, ky, kz, _ = _shells(n)
+    div = (kx * np.fft.fftn(u) + ky * np.fft.fftn(v) + kz * np.fft.fftn(w)) / float(n) ** 3
+    return float(np.max(np.abs(div)))
+
+
 def velocity(fields: FieldSet):
     """Interior velocity (m/rho) tensors of a device FieldSet."""
     it = fields.interior()

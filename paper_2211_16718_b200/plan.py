@@ -172,6 +172,15 @@ class Plan:
         ``out`` (fused into the last z sweep in fast mode; hd_arm_reduce)."""
         _lib.check(self.L.hd_arm_reduce(self.h, _ptr(out), tag), "hd_arm_reduce")
 
+    def enstrophy(self, u, out) -> None:
+        """out[0] = sum over the interior of 0.5 |curl(m/rho)|^2 (ghosts of u valid)."""
+        _lib.check(self.L.hd_enstrophy(self.h, _ptr(u), _ptr(out), _stream_ptr()), "hd_enstrophy")
+
+    def arm_enstrophy(self, out) -> None:
+        """The next step also writes the enstrophy sum of its start state to ``out``
+        (folded into the stage-0 viscous flux kernel; hd_arm_enstrophy)."""
+        _lib.check(self.L.hd_arm_enstrophy(self.h, _ptr(out)), "hd_arm_enstrophy")
+
     def set_dt(self, red, cfl_mode: int, cfl: float, dt_fixed: float, t_final: float, ctx,
                tag: int) -> None:
         _lib.check(self.L.hd_set_dt(self.h, _ptr(red) if red is not None else ctypes.c_void_p(None),
@@ -265,7 +274,13 @@ def error_from_key(key: int, spec: GridSpec, step_base: int = 0, wrap_steps: boo
     stage = slot - 1
     g = spec.ghost_width
     gx, gy = spec.n[0] + 2 * g, spec.n[1] + 2 * g
-    where = (point // (gx * gy), (point // gx) % gy, point % gx)  # (z, y, x) array index
+    where = (point // (gx * gy), (point // gx) % gy, point % gx)  # (z, y, x) ghosted index
+    if not (1 <= slot <= 4):
+        # the CFL reduction / step diagnostics decode the interior only
+        # (timeint.py:110-112 cons_to_prim on fields.interior()): interior index
+        where = tuple(c - g for c in where)
+    # RK stages: the first copy in C order over the filled ghosted box, as the
+    # reference's decode_primitives reports it (kernels latch first_image)
     kind = "density" if code == 1 else "pressure"
     inner = InvalidStateError(f"nonpositive {kind} at array index {where}", where=where)
     if not (1 <= slot <= 4) or not wrap_steps:

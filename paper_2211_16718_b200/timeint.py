@@ -81,6 +81,7 @@ class StepRecord:
     max_wavespeed: float
     wall_seconds: float
     kinetic_energy: float = float("nan")  # 0.5 <|m/rho|^2>: compute_spectrum().total() by Parseval
+    enstrophy: float = float("nan")  # 0.5 <|curl(m/rho)|^2>, 4th-order central differences
 
     def log_line(self) -> str:
         mx, my, mz = self.momentum
@@ -144,6 +145,18 @@ def kinetic_energy(fields: FieldSet, gas: GasModel = GasModel()) -> float:
     """Mean 0.5|m/rho|^2 over the interior = hit.compute_spectrum(...).total()."""
     r = _reduce(_as_device(fields), gas)
     return float(r[_lib.HD_RED_KE]) / fields.spec.interior_points
+
+
+def enstrophy(fields: FieldSet, gas: GasModel = GasModel()) -> float:
+    """Mean 0.5|curl v|^2 over the interior, v = m * (1/rho) (physics.py:249-252),
+    each derivative the reference's central_derivative_4 (viscous.py:23-51).
+    Refills the ghost layers of ``fields`` first (periodic), like the rhs does."""
+    fs = _as_device(fields)
+    plan = get_plan(fs.spec, gas)
+    plan.fill_ghosts(fs.data, 5)
+    out = torch.empty(1, dtype=torch.float64, device=fs.data.device)
+    plan.enstrophy(fs.data, out)
+    return float(out.item()) / fs.spec.interior_points
 
 
 def max_signal(fields: FieldSet, gas: GasModel, cfl_mode: str = "max") -> float:
@@ -262,6 +275,9 @@ class _Records:
         self.n += 1
 
 
+ENS_COL = 2 + _lib.HD_RED_ENSTROPHY  # enstrophy sum in a record row
+
+
 def _record(step: int, row: np.ndarray, spec: GridSpec, wall: float, points: int) -> StepRecord:
     vol = spec.cell_volume()
     red = row[2:]
@@ -273,6 +289,7 @@ def _record(step: int, row: np.ndarray, spec: GridSpec, wall: float, points: int
         max_wavespeed=float(red[_lib.HD_RED_WAVESPEED]),
         wall_seconds=wall,
         kinetic_energy=float(red[_lib.HD_RED_KE]) / points,
+        enstrophy=float(row[ENS_COL]) / points,
     )
 
 
@@ -307,7 +324,7 @@ class _DeviceMarch:
 
     def __init__(self, plan, fields: FieldSet, gas: GasModel, tparams: TimeParams, t0: float,
                  stepper=None, reducer=None, global_points: int | None = None, copy: bool = True,
-                 error_combine=None):
+                 error_combine=None, ghost_sync=None, sum_combine=None):
         self.plan = plan
         self.spec = fields.spec
         # interior points of the whole (possibly decomposed) domain: the KE mean
@@ -320,13 +337,22 @@ class _DeviceMarch:
         self.ctx = plan.ctx
         self.ctx.zero_()
         self.ctx[_lib.HD_CTX_T] = self.t0
-        self.red = torch.empty(_lib.HD_RED_N, dtype=torch.float64, device=dev)
+        self.red = torch.zeros(_lib.HD_RED_N, dtype=torch.float64, device=dev)
         self.scheme = _SCHEME_CODE[tparams.scheme]
         # multi-rank drivers override how a step runs and how reductions combine
         self.own_stepper = stepper is None and reducer is None
         self.stepper = stepper or (lambda u, dt_dev, tag: plan.step(self.scheme, u, dt_dev, tag))
         self.reducer = reducer or (lambda red: None)
         self.error_combine = error_combine or (lambda key: key)
+        # ghosts of the march state valid again after the last step (decomposed runs:
+        # the final halo), and the rank sum of per-rank partial sums
+        self.ghost_sync = ghost_sync or (lambda u: None)
+        self.sum_combine = sum_combine or (lambda t: None)
+
+    def _enstrophy_now(self, dst: torch.Tensor) -> None:
+        """Enstrophy sum of the current state into ``dst`` (one element)."""
+        self.ghost_sync(self.out.data)
+        self.plan.enstrophy(self.out.data, dst)
 
     def _reduce(self, tag: int) -> None:
         self.plan.reduce(self.out.data, self.red, tag)
@@ -384,6 +410,7 @@ class _DeviceMarch:
         def record(k):
             rows[k, 0:2] = self.ctx[0:2]
             rows[k, 2:] = self.red
+            plan.enstrophy(self.out.data, rows[k, ENS_COL:ENS_COL + 1])
 
         if tp.dt is None:
             self._reduce(0)
@@ -400,6 +427,7 @@ class _DeviceMarch:
                 self._one_step(1 + r, r, cfl_mode)
                 chunk_rows[r, 0:2] = self.ctx[0:2]
                 chunk_rows[r, 2:] = self.red
+                plan.enstrophy(self.out.data, chunk_rows[r, ENS_COL:ENS_COL + 1])
         torch.cuda.current_stream(dev).wait_stream(side)
         for c in range(nchunks):
             graph.replay()
@@ -455,8 +483,11 @@ class _DeviceMarch:
                     self._reduce(tag_pre)
                 plan.set_dt(self.red, cfl_mode, tp.cfl, 0.0, t_final, self.ctx, tag_pre)
             # diagnostics of the new state (= next step's CFL signal), fused into the last
-            # RK stage's update kernel when the plan can (hd_arm_reduce)
+            # RK stage's update kernel when the plan can (hd_arm_reduce); the enstrophy of
+            # the previous step's result, folded into this step's first flux kernel
             plan.arm_reduce(self.red, step * 8 + 7)
+            if step >= 1 and not sync_each:
+                plan.arm_enstrophy(recs.rows[step - 1, ENS_COL:ENS_COL + 1])
             self.stepper(self.out.data, self.ctx[_lib.HD_CTX_DT:], step)
             plan.commit_time(self.ctx)
             self.reducer(self.red)
@@ -464,6 +495,9 @@ class _DeviceMarch:
             recs.push(self.ctx, self.red)
             step += 1
             if sync_each:
+                ens = recs.rows[step - 1, ENS_COL:ENS_COL + 1]
+                self._enstrophy_now(ens)
+                self.sum_combine(ens)
                 row = recs.rows[step - 1].cpu().numpy()
                 self._check(step_base=0)
                 t = float(row[0])
@@ -473,6 +507,11 @@ class _DeviceMarch:
                 if observer is not None:
                     observer(rec)
         if not sync_each:
+            if step:
+                self._enstrophy_now(recs.rows[step - 1, ENS_COL:ENS_COL + 1])
+                ens = recs.rows[: recs.n, ENS_COL].contiguous()
+                self.sum_combine(ens)
+                recs.rows[: recs.n, ENS_COL] = ens
             rows = recs.rows[: recs.n].cpu().numpy()
             self._check(step_base=0)
             total = _time.perf_counter() - last_wall

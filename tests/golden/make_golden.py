@@ -22,7 +22,9 @@ Fixtures (tests/golden/):
                 cases on a ragged (9, 5, 3) grid (all bitwise equal) and the
                 canonical values of bench.make_bench_values
   traj32.json   config 1 (32^3, RK4, CFL 0.4, mu=0.006, 10 steps): IC and
-                final SHA-256, per-variable L2, dts, KE per step
+                final SHA-256, per-variable L2, dts, KE per step,
+                enstrophy per step (the north star's diagnostic, built from the
+                reference's decode_primitives + central_derivative_4)
   viscous_limit.json  16^3 HIT, RK4, CFL 0.4 at mu = 0.3 (dt beyond the viscous
                 operator's RK4 limit): the StepError step / stage / kind the
                 reference raises; at mu = 0.2: 60 steps complete, final t and dts
@@ -142,13 +144,29 @@ def trajectory16():
     )
 
 
+def enstrophy(fields) -> float:
+    """0.5 <|curl v|^2> with the reference's own operators: velocities from
+    decode_primitives (physics.py:240-255), each derivative central_derivative_4
+    (viscous.py:23-51)."""
+    fs = fields.copy()
+    hd.fill_ghosts_periodic(fs)
+    _, u, v, w, _ = hd.decode_primitives(fs, 1.4)
+    h, g = fs.spec.spacing, fs.spec.ghost_width
+
+    def D(a, d):
+        return hd.central_derivative_4(a, d, h[d], g)
+
+    wx, wy, wz = D(w, 1) - D(v, 2), D(u, 2) - D(w, 0), D(v, 0) - D(u, 1)
+    return float(np.mean(0.5 * ((wx * wx + wy * wy) + wz * wz)))
+
+
 def trajectory32():
     spec = hd.GridSpec((32, 32, 32))
     ic = hd.make_initial_condition(spec, hd.HitParams())
     gas = hd.GasModel(mu=MU)
     fields = ic.copy()
     t = 0.0
-    dts, kes = [], []
+    dts, kes, ens = [], [], [enstrophy(ic)]
     it = ic.interior()
     kes.append(hd.compute_spectrum(it[1] / it[0], it[2] / it[0], it[3] / it[0]).total())
     for _ in range(10):
@@ -157,6 +175,7 @@ def trajectory32():
         dts.append(res.records[0].dt)
         it = fields.interior()
         kes.append(hd.compute_spectrum(it[1] / it[0], it[2] / it[0], it[3] / it[0]).total())
+        ens.append(enstrophy(fields))
     final = fields.interior()
     doc = {
         "config": "32^3 HIT IC (HitParams defaults, seed 2024), GasModel(mu=0.006), RK4, CFL 0.4, 10 steps",
@@ -166,6 +185,7 @@ def trajectory32():
         "t": t,
         "dt": dts,
         "ke": kes,
+        "enstrophy": ens,
         "l2": [float(np.sqrt(np.sum(final[v] ** 2))) for v in range(5)],
         "mass": res.records[0].mass,
         "energy": res.records[0].energy,
@@ -211,6 +231,9 @@ if __name__ == "__main__":
 
     if _sys.argv[1:] == ["bench_weights"]:
         bench_weights()
+        raise SystemExit(0)
+    if _sys.argv[1:] == ["trajectory32"]:
+        trajectory32()
         raise SystemExit(0)
     if _sys.argv[1:] == ["viscous_limit"]:
         viscous_limit()

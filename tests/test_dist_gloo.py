@@ -119,9 +119,19 @@ def test_decompose_and_numbering():
     assert lays[0].neighbor(2, -1) == 3 and lays[3].neighbor(2, +1) == 0
     assert hd.rank_of((1, 0, 2), (2, 2, 3)) == 1 + 2 * (0 + 2 * 2)
     assert hd.coords_of(9, (2, 2, 3)) == (1, 0, 2)
-    assert hd.default_dims(8, (512, 512, 512)) == (1, 1, 8)
+    # the reference's choice (pkg/tests/test_decomp.py:55-69): least face area, ties to x
+    n = (16, 16, 16)
+    assert hd.default_dims(1, n) == (1, 1, 1)
+    assert hd.default_dims(2, n) == (2, 1, 1)
+    assert hd.default_dims(4, n) == (4, 1, 1)
+    assert hd.default_dims(8, n) == (4, 2, 1)
+    assert hd.default_dims(8, (16, 16, 16), 3) == (4, 2, 1)
     with pytest.raises(hd.ConfigError):
-        hd.default_dims(4, (64, 64, 8))  # local z extent 2 < ghost width
+        hd.default_dims(7, (16, 16, 16))  # 7 divides no extent
+    # the drivers' GPU default: z slabs when legal, else the reference's choice
+    assert hd.gpu_dims(8, (512, 512, 512)) == (1, 1, 8)
+    assert hd.gpu_dims(4, (64, 64, 8)) == (4, 1, 1)  # local z extent 2 < ghost width
+    assert hd.gpu_dims(8, (16, 16, 16)) == (4, 2, 1)
     with pytest.raises(hd.ConfigError):
         hd.decompose(spec, (1, 1, 3))
     with pytest.raises(hd.ConfigError):

@@ -36,7 +36,17 @@ for dims in json.loads(os.environ["HD_TEST_DIMS"]):
     fin = res.fields.interior().cpu().numpy()
     if rank == 0:
         print("RESULT " + json.dumps({"dims": dims, "sha": hashlib.sha256(fin.tobytes()).hexdigest(),
-                                      "t": res.t, "l2": [float(np.sqrt((fin[v] ** 2).sum())) for v in range(5)]}))
+                                      "t": res.t, "l2": [float(np.sqrt((fin[v] ** 2).sum())) for v in range(5)],
+                                      "reports": [[r.rank, r.wall_seconds, r.comp_seconds, r.comm_seconds]
+                                                  for r in res.reports]}))
+# per-step records of the block march (z slabs): KE and enstrophy summed over ranks
+lay = hd.decompose(spec, (1, 1, world))[rank]
+local = hd.scatter(ic, [lay])[0]
+res = hd.DistHalo(lay).advance(local, hd.GasModel(mu=0.006), hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=10),
+                               hd.DEFAULT_PARAMS, 0.0, 0.0, None, None, mode)
+if rank == 0:
+    print("RECORDS " + json.dumps({"ke": [r.kinetic_energy for r in res.records],
+                                   "enstrophy": [r.enstrophy for r in res.records]}))
 dist.destroy_process_group()
 '''
 
@@ -56,7 +66,9 @@ def _run(world, mode, tmp_path, dims=None, peer="1"):
     assert out.returncode == 0, out.stderr[-3000:]
     res = [json.loads(l[7:]) for l in out.stdout.splitlines() if l.startswith("RESULT ")]
     assert [tuple(r["dims"]) for r in res] == [tuple(d) for d in dims]
-    return res
+    recs = [json.loads(l[8:]) for l in out.stdout.splitlines() if l.startswith("RECORDS ")]
+    assert len(recs) == 1
+    return res, recs[0]
 
 
 @pytest.mark.parametrize("mode", ["exact", "fast"])
@@ -64,14 +76,23 @@ def test_decomposed_equals_single_gpu(tmp_path, traj32_golden, mode):
     ngpu = torch.cuda.device_count()
     if ngpu < 2:
         pytest.skip("needs >= 2 GPUs")
+    import numpy as np
+
     for world in [w for w in (2, 4) if w <= ngpu]:
-        for r in _run(world, mode, tmp_path):
+        res, recs = _run(world, mode, tmp_path)
+        # diagnostics of the decomposed march: KE curve and enstrophy (combined over ranks)
+        assert np.allclose(recs["ke"], traj32_golden["ke"][1:], rtol=1e-11, atol=0)
+        assert np.allclose(recs["enstrophy"], traj32_golden["enstrophy"][1:], rtol=1e-11, atol=0)
+        for r in res:
+            # one TimingReport per rank; comm = exposed halo/collective waits (> 0: every
+            # step waits for the dt reduction), comp = wall - comm
+            assert [q[0] for q in r["reports"]] == list(range(world))
+            for _, wall, comp, comm in r["reports"]:
+                assert 0.0 < comm < wall and abs(comp + comm - wall) <= 1e-9 * wall
             if mode == "exact":
                 assert r["sha"] == traj32_golden["final_sha256"], r["dims"]
                 assert r["t"] == traj32_golden["t"]
             else:
-                import numpy as np
-
                 l2 = np.array(r["l2"])
                 want = np.array(traj32_golden["l2"])
                 assert np.all(np.abs(l2 - want) / want <= 1e-10), r["dims"]
@@ -84,8 +105,12 @@ def test_z_slab_nccl_halo_equals_single_gpu(tmp_path, traj32_golden):
     if ngpu < 2:
         pytest.skip("needs >= 2 GPUs")
     world = 4 if ngpu >= 4 else 2
-    for r in _run(world, "exact", tmp_path, dims=[(1, 1, world)], peer="0"):
+    res, recs = _run(world, "exact", tmp_path, dims=[(1, 1, world)], peer="0")
+    for r in res:
         assert r["sha"] == traj32_golden["final_sha256"], r["dims"]
+    import numpy as np
+
+    assert np.allclose(recs["enstrophy"], traj32_golden["enstrophy"][1:], rtol=1e-11, atol=0)
 
 
 TF_SCRIPT = r'''

@@ -165,6 +165,30 @@ def test_config1_trajectory(hd, traj32_golden, mode):
         assert res.t == G["t"]
     assert np.all(np.abs(l2 - np.array(G["l2"])) / np.array(G["l2"]) <= TRAJ_TOL)
     assert np.allclose(ke, G["ke"][1:], rtol=1e-11, atol=0)
+    # enstrophy per step (north star; golden from the reference's operators): the
+    # previous step's result folded into each step's first flux kernel, the last
+    # one a separate pass
+    ens = [r.enstrophy for r in res.records]
+    assert np.allclose(ens, G["enstrophy"][1:], rtol=1e-11, atol=0)
+    assert abs(hd.enstrophy(ic) - G["enstrophy"][0]) <= 1e-12 * G["enstrophy"][0]
+
+
+@pytest.mark.parametrize("mu", [0.006, 0.0])
+def test_enstrophy_paths_agree(hd, mu):
+    """Folded into the stage-0 flux kernel (eager march), the stand-alone pass
+    (observer march, inviscid runs, final state) and the public function agree."""
+    spec = hd.GridSpec((32, 32, 32))
+    ic = hd.make_initial_condition(spec, hd.HitParams(), backend="numpy")
+    tp = hd.TimeParams(scheme="rk4", cfl=0.4, max_steps=4)
+    gas = hd.GasModel(mu=mu)
+    a = hd.advance(ic, gas, tp)
+    seen = []
+    b = hd.advance(ic, gas, tp, observer=seen.append)
+    ea = np.array([r.enstrophy for r in a.records])
+    eb = np.array([r.enstrophy for r in b.records])
+    assert np.all(np.isfinite(ea)) and len(seen) == 4
+    assert np.allclose(ea, eb, rtol=1e-13, atol=0)
+    assert np.isclose(hd.enstrophy(a.fields), ea[-1], rtol=1e-13, atol=0)
 
 
 def test_fast_vs_exact_32(hd):
@@ -227,6 +251,13 @@ def test_viscous_time_step_limit_fails_like_the_reference(hd, viscous_limit_gold
     assert "pressure" in str(ge.value)
     if mode == "exact":
         assert ge.value.step == bad["step"]
+        # the same array index as the reference: the first offending cell in C order
+        # over the filled ghosted box -- here a ghost image (z = 0)
+        inner = ge.value
+        while not hasattr(inner, "where"):
+            inner = inner.__cause__
+        assert tuple(int(c) for c in inner.where) == (0, 8, 9)
+        assert f"at array index {inner.where}" in str(ge.value)
     else:
         assert abs(ge.value.step - bad["step"]) <= 1
     res = hd.advance(ic, hd.GasModel(mu=ok["mu"]),

@@ -82,6 +82,8 @@ def test_error_key_decoding():
     # slot 0 / 7 (CFL reduction, diagnostics) -> InvalidStateError, not StepError
     err = error_from_key(((4 * 8 + 7) << 36) | (1 << 34) | point, spec)
     assert isinstance(err, hd.InvalidStateError) and not isinstance(err, hd.StepError)
+    # ... whose `where` is an interior index (cons_to_prim on fields.interior())
+    assert err.where == (4, 3, 2)
     err = error_from_key((7 << 36) | (3 << 34), spec)
     assert "dt" in str(err)
 
