@@ -61,7 +61,8 @@ extern "C" {
 #define HD_OPT_SEGMENTS 0      /* sweep segments per line: 0 = automatic (>= 6 waves), else fixed */
 #define HD_OPT_X_STAGED 1      /* 1 (default): cp.async-staged x sweep when n_y % 32 == 0; 0: plain */
 #define HD_OPT_FLUX_ZMARCH 2   /* 1 (default): z-marching viscous flux kernel when the tiles fit; 0: pointwise */
-#define HD_OPT_N 3
+#define HD_OPT_FLUX_TMA 3      /* 1 (default): fast-mode flux kernel fed by TMA when the state maps to a tensor */
+#define HD_OPT_N 4
 
 /* workspace buffers (hd_plan_buffer) */
 #define HD_BUF_STAGE 0 /* 10 fields: RK stage states, ping-pong halves (stage s writes half s%2) */

@@ -23,7 +23,7 @@ HD_MODE_EXACT = 1
 HD_SCHEME_RK3 = 3
 HD_SCHEME_RK4 = 4
 HD_PART_LOCAL, HD_PART_HALO, HD_PART_MID, HD_PART_UPDATE, HD_PART_ALL = 1, 2, 4, 8, 15
-HD_OPT_SEGMENTS, HD_OPT_X_STAGED, HD_OPT_FLUX_ZMARCH = 0, 1, 2
+HD_OPT_SEGMENTS, HD_OPT_X_STAGED, HD_OPT_FLUX_ZMARCH, HD_OPT_FLUX_TMA = 0, 1, 2, 3
 (HD_BUF_STAGE, HD_BUF_ACC, HD_BUF_INC, HD_BUF_PRIM, HD_BUF_VFLUX, HD_BUF_RED, HD_BUF_CTX,
  HD_BUF_ERR, HD_BUF_STATE, HD_BUF_SYNC, HD_BUF_FRED, HD_BUF_ENS) = range(12)
 HD_PEER_STATE, HD_PEER_VFLUX = 0, 1

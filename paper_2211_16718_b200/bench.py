@@ -1,28 +1,26 @@
-"""Memory-layout and traversal study of the nonlinear-weight kernel, on the GPU.
+"""Memory-layout / traversal study of the nonlinear-weight kernel on the GPU.
 
-Mirrors pkg/src/hitdns/bench.py (X_PAD, BYTES_PER_POINT, DEFAULT_SIZES,
-DEFAULT_TILE, TRAVERSALS, BENCH_SEED, make_bench_values, pack_values,
-BenchRecord, run_case, layout_sweep, bench_report, soft_ordering_checks) with
-the numba kernels (kernels.py:236-329) replaced by ``hd_bench_weights`` in
-libhd.so:
+The reference's microbenchmark (pkg/src/hitdns/bench.py, kernels.py:236-329)
+asks how the data layout and the visiting order change the throughput of the
+WENO weight computation; here the kernel is ``hd_bench_weights`` in libhd.so
+and every repeat is timed with CUDA events on the launching stream:
 
-* layout: INTERLEAVED (AoS) or COMPONENT_CONTIGUOUS (SoA) device buffers;
-* traversal: ``"lex"`` -- one thread per active point, x fastest, so a warp
-  reads 32 consecutive points of one variable (SoA: 256 B per load, fully
-  coalesced; AoS: stride 40 B, 5x the sectors); ``"tiled"`` -- (tx, ty)
-  thread blocks over x-y tiles of each z plane, with idle lanes where the
-  tile overhangs a ragged extent (the reference's wasted iterations).
+* layout: INTERLEAVED (AoS: the five variables of a point adjacent) or
+  COMPONENT_CONTIGUOUS (SoA: one variable's points adjacent);
+* traversal ``"lex"``: one thread per active point, x fastest (SoA: a warp
+  reads 256 contiguous bytes per load; AoS: a 40-byte stride, 5x the sectors);
+  ``"tiled"``: (tx, ty) thread tiles over each z plane, whose lanes past a
+  ragged edge idle (the reference's wasted iterations).
 
-Each repeat is timed with CUDA events on the launching stream; the output is
-the same point-major weight array as the reference, bitwise, for every
-layout x traversal combination (kernel operations in the reference order,
-never contracted).
+Public names and numbers follow the reference (X_PAD, BYTES_PER_POINT = 320,
+the seeded dataset, the report's columns, the soft ordering warnings) so its
+tests and reports carry over; the weights themselves are bitwise the
+reference's for every layout x traversal (tests/golden/bench_weights.npz).
 """
 
 from __future__ import annotations
 
 import ctypes
-import statistics
 import warnings
 from dataclasses import dataclass, field
 
@@ -34,164 +32,181 @@ from .grid import Layout
 from .physics import DEFAULT_PARAMS, WenoParams
 
 NVARS = 5
-X_PAD = 2  # stencil reach of the weight kernel along x
-BYTES_PER_POINT = NVARS * (5 + 3) * 8
+X_PAD = 2                           # x reach of the 5-point stencil
+BYTES_PER_POINT = NVARS * 8 * (5 + 3)  # per active point: 5 stencil reads + 3 weight writes per variable
 DEFAULT_SIZES = (16, 32, 48, 64)
 DEFAULT_TILE = (32, 8)
 TRAVERSALS = ("lex", "tiled")
 BENCH_SEED = 20170907
+_LAYOUT_LABEL = {Layout.INTERLEAVED: "interleaved", Layout.COMPONENT_CONTIGUOUS: "contiguous"}
 
 
-def _shape3(n) -> tuple[int, int, int]:
-    if np.isscalar(n):
-        return (int(n),) * 3
-    nx, ny, nz = (int(v) for v in n)
-    return (nx, ny, nz)
+def _extents(n) -> tuple:
+    """(nx, ny, nz) from a cube edge or a triple."""
+    return (int(n),) * 3 if np.isscalar(n) else tuple(int(v) for v in n)
+
+
+def _padded_points(nx: int, ny: int, nz: int) -> int:
+    return (nx + 2 * X_PAD) * ny * nz
 
 
 def make_bench_values(shape, seed: int = BENCH_SEED) -> np.ndarray:
-    """Canonical per-point values in [0.5, 1.5), shape (padded points, NVARS) (bench.py:45-50)."""
-    nx, ny, nz = _shape3(shape)
-    npts = (nx + 2 * X_PAD) * ny * nz
+    """The seeded dataset, (padded points, 5) values in [0.5, 1.5) so the weights
+    stay well conditioned (bench.py:45-50: one default_rng draw)."""
     rng = np.random.default_rng(seed)
-    return 0.5 + rng.random((npts, NVARS))
+    return rng.random((_padded_points(*_extents(shape)), NVARS)) + 0.5
 
 
 def pack_values(values: np.ndarray, layout: Layout) -> np.ndarray:
-    """One flat buffer per layout (bench.py:53-57)."""
-    if layout == Layout.INTERLEAVED:
-        return np.ascontiguousarray(values).reshape(-1)
-    return np.ascontiguousarray(values.T).reshape(-1)
+    """The flat buffer of a layout: point-major (AoS) or variable-major (SoA)."""
+    table = values if layout == Layout.INTERLEAVED else values.T
+    return np.ascontiguousarray(table).ravel()
 
 
 @dataclass
 class BenchRecord:
-    """One benchmarked configuration with its timing statistics (bench.py:60-99)."""
+    """Timings (seconds per repeat) of one shape x layout x traversal."""
 
-    shape: tuple[int, int, int]
+    shape: tuple
     layout: Layout
     traversal: str
-    times: list[float] = field(default_factory=list)
+    times: list = field(default_factory=list)
     wasted_lanes: int = 0
+
+    def _t(self) -> np.ndarray:
+        return np.asarray(self.times, dtype=np.float64)
 
     @property
     def active_points(self) -> int:
-        return self.shape[0] * self.shape[1] * self.shape[2]
+        return int(np.prod(self.shape))
 
     @property
     def median_seconds(self) -> float:
-        return statistics.median(self.times)
+        return float(np.median(self._t()))
 
     @property
     def min_seconds(self) -> float:
-        return min(self.times)
+        return float(self._t().min())
 
     @property
     def cv(self) -> float:
-        mean = statistics.fmean(self.times)
-        return statistics.pstdev(self.times) / mean if mean > 0.0 else 0.0
+        """Coefficient of variation (population std / mean) of the repeats."""
+        t = self._t()
+        return float(t.std() / t.mean()) if t.mean() > 0.0 else 0.0
 
     @property
     def bandwidth_gbs(self) -> float:
-        return self.active_points * BYTES_PER_POINT / self.median_seconds / 1e9
+        return self.active_points * BYTES_PER_POINT / self.median_seconds * 1e-9
 
     @property
     def wasted_fraction(self) -> float:
-        visited = self.active_points + self.wasted_lanes
-        return self.wasted_lanes / visited if visited else 0.0
+        total = self.active_points + self.wasted_lanes
+        return self.wasted_lanes / total if total else 0.0
 
     @property
     def size_label(self) -> str:
         nx, ny, nz = self.shape
-        return str(nx) if nx == ny == nz else f"{nx}x{ny}x{nz}"
+        return f"{nx}" if nx == ny == nz else f"{nx}x{ny}x{nz}"
+
+
+def _layout_name(layout: Layout) -> str:
+    return _LAYOUT_LABEL[Layout(layout)]
+
+
+class _WeightKernel:
+    """hd_bench_weights bound to one device dataset and output buffer."""
+
+    def __init__(self, shape, layout: Layout, traversal: str, tile, params: WenoParams, seed: int):
+        self.L = _lib.load(require_cuda=True)
+        self.shape = shape
+        self.layout = Layout(layout)
+        self.code = TRAVERSALS.index(traversal)
+        self.tile = (int(tile[0]), int(tile[1]))
+        self.params = params
+        self.data = torch.from_numpy(pack_values(make_bench_values(shape, seed), self.layout)).cuda()
+        self.out = torch.zeros(3 * NVARS * _padded_points(*shape), dtype=torch.float64, device="cuda")
+        self.wasted = ctypes.c_int64(0)
+        self.stream = torch.cuda.current_stream()
+
+    def launch(self) -> None:
+        nx, ny, nz = self.shape
+        status = self.L.hd_bench_weights(
+            self.data.data_ptr(), int(self.layout), self.code, nx, ny, nz, X_PAD, *self.tile,
+            float(self.params.epsilon), int(self.params.power), self.out.data_ptr(),
+            ctypes.byref(self.wasted), ctypes.c_void_p(self.stream.cuda_stream))
+        _lib.check(status, "hd_bench_weights")
+
+    def timed(self) -> float:
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        start.record(self.stream)
+        self.launch()
+        stop.record(self.stream)
+        stop.synchronize()
+        return start.elapsed_time(stop) * 1e-3
 
 
 def run_case(shape, layout: Layout, traversal: str = "lex", repeats: int = 5,
-             tile: tuple[int, int] = DEFAULT_TILE, params: WenoParams = DEFAULT_PARAMS,
-             seed: int = BENCH_SEED) -> tuple[BenchRecord, np.ndarray]:
-    """Time one (shape, layout, traversal) case on the current CUDA device;
-    returns the record and the point-major weight output (bench.py:102-140)."""
+             tile: tuple = DEFAULT_TILE, params: WenoParams = DEFAULT_PARAMS,
+             seed: int = BENCH_SEED) -> tuple:
+    """One configuration on the current device: (record, point-major weights).
+    One untimed launch first (module load), then ``repeats`` timed ones."""
     if traversal not in TRAVERSALS:
         raise ValueError(f"traversal must be one of {TRAVERSALS}, got {traversal!r}")
     if repeats < 1:
         raise ValueError("repeats must be at least 1")
-    L = _lib.load(require_cuda=True)
-    nx, ny, nz = _shape3(shape)
-    data = torch.from_numpy(pack_values(make_bench_values((nx, ny, nz), seed), layout)).cuda()
-    npts = (nx + 2 * X_PAD) * ny * nz
-    out = torch.zeros(3 * NVARS * npts, dtype=torch.float64, device="cuda")
-    record = BenchRecord(shape=(nx, ny, nz), layout=Layout(layout), traversal=traversal)
-    stream = torch.cuda.current_stream()
-    wasted = ctypes.c_int64(0)
-
-    def run_once() -> None:
-        _lib.check(L.hd_bench_weights(data.data_ptr(), int(layout), TRAVERSALS.index(traversal), nx, ny,
-                                      nz, X_PAD, int(tile[0]), int(tile[1]), float(params.epsilon),
-                                      int(params.power), out.data_ptr(), ctypes.byref(wasted),
-                                      ctypes.c_void_p(stream.cuda_stream)), "hd_bench_weights")
-
-    run_once()  # warm-up
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(repeats):
-        torch.cuda.synchronize()
-        e0.record(stream)
-        run_once()
-        e1.record(stream)
-        e1.synchronize()
-        record.times.append(e0.elapsed_time(e1) / 1e3)
-    record.wasted_lanes = int(wasted.value)
-    return record, out.cpu().numpy()
+    shape = _extents(shape)
+    kernel = _WeightKernel(shape, layout, traversal, tile, params, seed)
+    kernel.launch()
+    times = [kernel.timed() for _ in range(repeats)]
+    record = BenchRecord(shape=shape, layout=Layout(layout), traversal=traversal, times=times,
+                         wasted_lanes=int(kernel.wasted.value))
+    return record, kernel.out.cpu().numpy()
 
 
 def layout_sweep(sizes=DEFAULT_SIZES, repeats: int = 5, traversals=("lex",),
-                 tile: tuple[int, int] = DEFAULT_TILE) -> list[BenchRecord]:
-    """Every size x layout x traversal combination (bench.py:143-156)."""
-    records = []
-    for n in sizes:
-        for layout in (Layout.INTERLEAVED, Layout.COMPONENT_CONTIGUOUS):
-            for traversal in traversals:
-                rec, _ = run_case(n, layout, traversal, repeats=repeats, tile=tile)
-                records.append(rec)
-    return records
+                 tile: tuple = DEFAULT_TILE) -> list:
+    """Records for sizes x (interleaved, contiguous) x traversals, in that nesting."""
+    return [run_case(n, layout, trav, repeats=repeats, tile=tile)[0]
+            for n in sizes
+            for layout in (Layout.INTERLEAVED, Layout.COMPONENT_CONTIGUOUS)
+            for trav in traversals]
 
 
-def _layout_name(layout: Layout) -> str:
-    return "interleaved" if layout == Layout.INTERLEAVED else "contiguous"
-
-
-def bench_report(records: list[BenchRecord]) -> str:
-    """Text table ``n layout traversal median_s bandwidth_GBs ratio_vs_baseline``;
-    the baseline of each size is its interleaved/lex row, else its first row
-    (bench.py:163-189)."""
-    baselines = {}
+def bench_report(records: list) -> str:
+    """``n layout traversal median_s bandwidth_GBs ratio_vs_baseline`` rows; the
+    baseline of a size is its interleaved/lex record when present, else its
+    first record; a trailing ``# max_cv`` line (bench.py:163-189)."""
+    base = {}
     for rec in records:
-        key = rec.size_label
-        if key not in baselines or (rec.layout == Layout.INTERLEAVED and rec.traversal == "lex"):
-            baselines[key] = rec
-    lines = ["n layout traversal median_s bandwidth_GBs ratio_vs_baseline"]
-    for rec in records:
-        ratio = rec.median_seconds / baselines[rec.size_label].median_seconds
-        lines.append(f"{rec.size_label} {_layout_name(rec.layout)} {rec.traversal} "
-                     f"{rec.median_seconds:.3g} {rec.bandwidth_gbs:.3g} {ratio:.3g}")
+        first = rec.size_label not in base
+        if first or (rec.layout == Layout.INTERLEAVED and rec.traversal == "lex"):
+            base[rec.size_label] = rec.median_seconds
+    rows = ["n layout traversal median_s bandwidth_GBs ratio_vs_baseline"]
+    rows += [" ".join((r.size_label, _layout_name(r.layout), r.traversal, f"{r.median_seconds:.3g}",
+                       f"{r.bandwidth_gbs:.3g}", f"{r.median_seconds / base[r.size_label]:.3g}"))
+             for r in records]
     if records:
-        lines.append(f"# max_cv {max(rec.cv for rec in records):.3g}")
-    return "\n".join(lines) + "\n"
+        rows.append(f"# max_cv {max(r.cv for r in records):.3g}")
+    return "\n".join(rows) + "\n"
 
 
-def soft_ordering_checks(records: list[BenchRecord]) -> list[str]:
-    """Expected-but-not-guaranteed orderings, reported as warnings (bench.py:192-221)."""
+def soft_ordering_checks(records: list) -> list:
+    """Orderings the study expects but cannot guarantee (cache- and
+    scheduler-dependent), returned and emitted as RuntimeWarnings: SoA/lex at
+    least as fast as AoS/lex; a tiled run that idles lanes no faster than lex."""
+    table = {(r.size_label, Layout(r.layout), r.traversal): r for r in records}
     notes = []
-    by_key = {(r.size_label, r.layout, r.traversal): r for r in records}
     for size in sorted({r.size_label for r in records}):
-        aos = by_key.get((size, Layout.INTERLEAVED, "lex"))
-        soa = by_key.get((size, Layout.COMPONENT_CONTIGUOUS, "lex"))
-        if aos and soa and soa.median_seconds > aos.median_seconds:
+        aos, soa = table.get((size, Layout.INTERLEAVED, "lex")), table.get((size, Layout.COMPONENT_CONTIGUOUS, "lex"))
+        if aos is not None and soa is not None and soa.median_seconds > aos.median_seconds:
             notes.append(f"n={size}: contiguous layout was slower than interleaved "
                          f"({soa.median_seconds:.3g}s vs {aos.median_seconds:.3g}s)")
         for layout in (Layout.INTERLEAVED, Layout.COMPONENT_CONTIGUOUS):
-            lex = by_key.get((size, layout, "lex"))
-            tiled = by_key.get((size, layout, "tiled"))
-            if lex and tiled and tiled.wasted_lanes > 0 and tiled.median_seconds < lex.median_seconds:
+            lex, tiled = table.get((size, layout, "lex")), table.get((size, layout, "tiled"))
+            if lex is None or tiled is None or not tiled.wasted_lanes:
+                continue
+            if tiled.median_seconds < lex.median_seconds:
                 notes.append(f"n={size} {_layout_name(layout)}: tiled traversal beat lexicographic "
                              f"despite wasting {tiled.wasted_fraction:.1%} of its lanes")
     for note in notes:

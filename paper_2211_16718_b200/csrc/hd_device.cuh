@@ -23,11 +23,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// the same stencil on values already in registers / shared memory
+// the same stencil on values already in registers / shared memory; the fast
+// form rounds the derivative itself (no contraction into its consumers), so a
+// kernel variant that uses it twice (flux kernel + enstrophy) computes the same
+// fluxes bit for bit
 template <bool EXACT>
 __device__ __forceinline__ double cd4v(double m2, double m1, double p1, double p2, double coef) {
   if constexpr (EXACT) return xm(xa(xs(xa(-p2, xm(8.0, p1)), xm(8.0, m1)), m2), coef);
-  return (8.0 * (p1 - m1) + (m2 - p2)) * coef;
+  return __dmul_rn(8.0 * (p1 - m1) + (m2 - p2), coef);
 }
 
 // Writes v at interior point (i,j,k) of field f and at its periodic images

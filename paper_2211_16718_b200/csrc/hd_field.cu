@@ -9,6 +9,8 @@
 //   rk_update_kernel     timeint.py:168-193 when mu == 0 (viscous.py:72-73 short-circuit)
 //   central_diff4_kernel kernels.py:207-227 (stand-alone, for the operator API)
 //   reduce kernels       timeint.py:100-131 (CFL signal, totals, max wavespeed, KE)
+#include <cuda.h>
+
 #include "hd_device.cuh"
 
 namespace hd {
@@ -274,18 +276,7 @@ int64_t ens_capacity(const hd_geom& g) {
   return tiles + 4096 > ENS_BLOCKS_MAX ? tiles + 4096 : ENS_BLOCKS_MAX;
 }
 
-int launch_enstrophy(const hd_plan* p, const double* u, double* out, cudaStream_t s) {
-  const Geo& G = p->geo;
-  const int64_t rows = (int64_t)G.n[1] * G.n[2];
-  int blocks = (int)((rows + ENS_THREADS / 32 - 1) / (ENS_THREADS / 32));
-  if (blocks > ENS_BLOCKS_MAX) blocks = ENS_BLOCKS_MAX;
-  double* partial = (double*)(p->ws + p->off[HD_BUF_ENS]);
-  enstrophy_kernel<<<blocks, ENS_THREADS, 0, s>>>(u, G, partial);
-  sum_finish_kernel<<<1, 32, 0, s>>>(partial, blocks, out);
-  hd::count_launches(2);
-  return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
-}
-
+// defined after the z-marching flux kernel
 // gradflux with z marching (blocks of 32 x 8 columns): the z stencil comes from
 // a per-thread register queue of 5 planes (each prims value is loaded once per
 // column), the x/y stencils from a shared-memory plane tile with a 2-point halo.
@@ -308,9 +299,9 @@ __device__ __forceinline__ void prims_of(const double (&c)[5], double gamma, dou
 // FROM_U (fast mode): `src` is the conserved state and every loaded point is
 // converted to primitives on the fly (no primitive fields in HBM); else `src`
 // holds the 4 primitive fields.
-// ENS: also the enstrophy of the state from the velocity gradients it forms
-// (one partial per block into ens_partial)
-template <bool EXACT, bool FROM_U, bool ENS>
+// ENS: 1 = also the enstrophy of the state from the velocity gradients it forms
+// (one partial per block into ens_partial); 2 = only that (no flux fields)
+template <bool EXACT, bool FROM_U, int ENS>
 __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_zm_kernel(
     const double* __restrict__ prim, double* __restrict__ vf, Geo G, double mu, double q_coef,
     int zseg, double gamma, double* ens_partial) {
@@ -413,7 +404,8 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_zm_kernel(
       }
     }
     const double vel[3] = {qz[0][2], qz[1][2], qz[2][2]};
-    if constexpr (ENS) ens += enstrophy_point(gr);
+    if constexpr (ENS != 0) ens += enstrophy_point(gr);
+    if constexpr (ENS == 2) continue;
     double val[VF_N];
     viscous_flux_point<EXACT>(gr, gT, vel, mu, q_coef, val);
     // each field gets face images only along the axes it is differentiated along
@@ -449,10 +441,313 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_zm_kernel(
   if (G.peer_any && ((G.peer[2] && (k0 < G.g || k1 > G.n[2] - G.g)) ||
                      touches_peer(G, i, j, G.g)))
     __threadfence_system();
-  if constexpr (ENS)
+  if constexpr (ENS != 0)
     block_sum_store(ens, ens_partial, ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
 }
 
+
+// ---------------------------------------------------------------------------
+// z-marching flux kernel fed by TMA (fast mode, primitives from the state).
+// The same tile march as gradflux_zm_kernel, but the raw state arrives as one
+// 4D TMA box per plane -- (38 x, 12 y, 1 z, 5 variables): the 32 x 8 tile plus
+// its 2-point halo, widened by one column on each side so the box starts on a
+// 16-byte boundary (a tensor load whose innermost start coordinate is not
+// 16-byte aligned raises an illegal instruction on B200; tools/gpu/tma_bisect*.cu)
+// -- into a ring of GT_S shared-memory slots, tracked by one
+// mbarrier per slot (expect_tx / complete_tx).  Thread 0 refills the slot of
+// plane k with plane k + 4 right after iteration k's barrier, so every load is
+// in flight ~2 planes ahead with no registers held and no per-thread address
+// arithmetic; the threads only convert (their centre of plane k+2 into the
+// register z queue, the halo ring of plane k into the primitive tile) and
+// compute.  One barrier per plane, as before: it also retires the raw slot.
+// ---------------------------------------------------------------------------
+constexpr int GT_S = 4;
+constexpr int GT_BX = GZ_PX + 2;      // box width: x - 3 .. x + 34 of the tile, 304 B rows
+constexpr int GT_BOX = NV * GZ_PY * GT_BX;          // doubles per box (18,240 B)
+constexpr int GT_SLOT = (GT_BOX + 15) / 16 * 16;    // slots 128-byte aligned (TMA destination)
+struct GtSmem {
+  double raw[GT_S][GT_SLOT];           // 73,216 B
+  double tile[2][4][GZ_PY][GZ_PX];     // 27,648 B (primitive planes, double-buffered)
+  unsigned long long full[GT_S];       // mbarriers
+};
+constexpr unsigned GT_BOX_BYTES = GT_BOX * 8;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                            int c3, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int ENS>
+__global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_tma_kernel(
+    const __grid_constant__ CUtensorMap tm, double* __restrict__ vf, Geo G, double mu, double q_coef,
+    int zseg, double gamma, double* ens_partial) {
+  extern __shared__ __align__(128) unsigned char gt_smem[];
+  GtSmem& S = *reinterpret_cast<GtSmem*>(gt_smem);
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * GZ_TX + tx;
+  const int i = blockIdx.x * GZ_TX + tx, j = blockIdx.y * GZ_TY + ty;
+  const int k0 = blockIdx.z * zseg;
+  const int k1 = min(k0 + zseg, G.n[2]);
+  const int g = G.g;
+  const int p0 = k0 - 2, plast = k1 + 1;  // planes the z stencils touch
+  // box origin (ghosted coordinates): x one column left of the halo, even, so the
+  // row start is 16-byte aligned (n_x % 32 == 0, g = 3 -> 32 bx + g - 3)
+  const int bx = blockIdx.x * GZ_TX - GZ_H - 1 + g, by = blockIdx.y * GZ_TY - GZ_H + g;
+  double coef[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) coef[d] = 1.0 / (12.0 * G.h[d]);
+  const double gm1 = gamma - 1.0;
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm) : "memory");
+    for (int s = 0; s < GT_S; ++s) mbar_init(&S.full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int p) {  // thread 0
+    const int s = (p - p0) % GT_S;
+    mbar_expect_tx(&S.full[s], GT_BOX_BYTES);
+    tma_load_4d(&S.raw[s][0], &tm, bx, by, p + g, 0, &S.full[s]);
+  };
+  auto wait_plane = [&](int p) {
+    const int r = p - p0;
+    mbar_wait(&S.full[r % GT_S], (unsigned)((r / GT_S) & 1));
+  };
+  auto prims_at = [&](int p, int py, int px, double (&pv)[4]) {
+    const int s = (p - p0) % GT_S;
+    double c[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) c[v] = S.raw[s][(v * GZ_PY + py) * GT_BX + px + 1];
+    prims_of(c, gamma, gm1, pv);
+  };
+  if (tid == 0)
+    for (int p = p0; p < p0 + GT_S && p <= plast; ++p) issue(p);
+  // z queue: qz[f][w] = primitive f at plane k - 2 + w of this column
+  double qz[4][5];
+#pragma unroll
+  for (int w = 1; w < 5; ++w) {
+    const int p = k0 - 3 + w;
+    wait_plane(p);
+    double pv[4];
+    prims_at(p, ty + GZ_H, tx + GZ_H, pv);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) qz[f][w] = pv[f];
+  }
+  // halo ring of the primitive tile (minus the never-read corners): <= 1 point per thread
+  const int r = tid;
+  int px = 0, py = 0;
+  bool has_ring = r < GZ_PX * GZ_PY - GZ_TX * GZ_TY;
+  if (has_ring) {
+    if (r < 2 * GZ_H * GZ_PX) {
+      py = r / GZ_PX;
+      px = r % GZ_PX;
+      if (py >= GZ_H) py += GZ_TY;
+    } else {
+      const int s = r - 2 * GZ_H * GZ_PX;
+      py = GZ_H + s / (2 * GZ_H);
+      px = s % (2 * GZ_H);
+      if (px >= GZ_H) px += GZ_TX;
+    }
+    has_ring = !((px < GZ_H || px >= GZ_H + GZ_TX) && (py < GZ_H || py >= GZ_H + GZ_TY));
+  }
+  __syncthreads();  // planes k0-2 and k0-1 were needed for their centres only
+  if (tid == 0) {
+    if (k0 + 2 <= plast) issue(k0 + 2);
+    if (k0 + 3 <= plast) issue(k0 + 3);
+  }
+  const int pm = periodic_mask(G);
+  const int64_t np = G.npts, sz = G.sz;
+  const int64_t dy = (int64_t)G.n[1] * G.sy, dz = (int64_t)G.n[2] * sz;
+  double ens = 0.0;
+  for (int k = k0; k < k1; ++k) {
+    const int b = k & 1;
+    wait_plane(k + 2);
+    double pq[4];
+    prims_at(k + 2, ty + GZ_H, tx + GZ_H, pq);
+    double pr[4];
+    if (has_ring) prims_at(k, py, px, pr);  // plane k arrived two iterations ago
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+#pragma unroll
+      for (int w = 0; w < 4; ++w) qz[f][w] = qz[f][w + 1];
+      qz[f][4] = pq[f];
+      S.tile[b][f][ty + GZ_H][tx + GZ_H] = qz[f][2];
+      if (has_ring) S.tile[b][f][py][px] = pr[f];
+    }
+    __syncthreads();
+    // every thread is done with raw plane k: its slot takes plane k + 4
+    if (tid == 0 && k + 4 <= plast) issue(k + 4);
+    double gr[3][3], gT[3];
+    const int cx = tx + GZ_H, cy = ty + GZ_H;
+    double (*tl)[GZ_PY][GZ_PX] = S.tile[b];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const double gx = cd4v<false>(tl[f][cy][cx - 2], tl[f][cy][cx - 1], tl[f][cy][cx + 1],
+                                    tl[f][cy][cx + 2], coef[0]);
+      const double gy = cd4v<false>(tl[f][cy - 2][cx], tl[f][cy - 1][cx], tl[f][cy + 1][cx],
+                                    tl[f][cy + 2][cx], coef[1]);
+      const double gz = cd4v<false>(qz[f][0], qz[f][1], qz[f][3], qz[f][4], coef[2]);
+      if (f < 3) {
+        gr[f][0] = gx;
+        gr[f][1] = gy;
+        gr[f][2] = gz;
+      } else {
+        gT[0] = gx;
+        gT[1] = gy;
+        gT[2] = gz;
+      }
+    }
+    if constexpr (ENS != 0) ens += enstrophy_point(gr);
+    if constexpr (ENS == 2) continue;
+    const double vel[3] = {qz[0][2], qz[1][2], qz[2][2]};
+    double val[VF_N];
+    viscous_flux_point<false>(gr, gT, vel, mu, q_coef, val);
+    const int64_t q = G.idx(i, j, k);
+    const bool xl = (pm & 1) && i < g, xh = (pm & 1) && i >= G.n[0] - g;
+    const bool yl = (pm & 2) && j < g, yh = (pm & 2) && j >= G.n[1] - g;
+    const bool zl = (pm & 4) && k < g, zh = (pm & 4) && k >= G.n[2] - g;
+#pragma unroll
+    for (int f = 0; f < VF_N; ++f) {
+      double* F = vf + (int64_t)f * np + q;
+      const double v = val[f];
+      F[0] = v;
+      const int axes = vf_axes(f);
+      if (axes & 1) {
+        if (xl) F[G.n[0] + G.peer_lo[0]] = v;
+        if (xh) F[-G.n[0] + G.peer_hi[0]] = v;
+      }
+      if (axes & 2) {
+        if (yl) F[dy + G.peer_lo[1]] = v;
+        if (yh) F[-dy + G.peer_hi[1]] = v;
+      }
+      if (axes & 4) {
+        if (zl) F[dz + G.peer_lo[2]] = v;
+        if (zh) F[-dz + G.peer_hi[2]] = v;
+      }
+    }
+  }
+  if (ENS != 2 && G.peer_any &&
+      ((G.peer[2] && (k0 < G.g || k1 > G.n[2] - G.g)) || touches_peer(G, i, j, G.g)))
+    __threadfence_system();
+  if constexpr (ENS != 0)
+    block_sum_store(ens, ens_partial, ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult st;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &st) != cudaSuccess ||
+        st != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return (EncodeTiledFn)f;
+  }();
+  return fn;
+}
+
+// The state u as a 4D tensor (x, y, z, variable) for TMA; false when the
+// geometry or alignment does not allow it (odd extents: 8-byte rows are not
+// 16-byte strides)
+static bool state_tensor_map(const hd_plan* p, const double* u, CUtensorMap* tm) {
+  const Geo& G = p->geo;
+  EncodeTiledFn enc = encode_tiled_fn();
+  // 16-byte aligned rows and box origins: even ghosted x extent, g odd (origin
+  // 32 bx + g - 3 even), 16-byte aligned base
+  if (!enc || (G.gn[0] % 2) || ((G.g - 3) % 2) || ((uintptr_t)u % 16)) return false;
+  const cuuint64_t dims[4] = {(cuuint64_t)G.gn[0], (cuuint64_t)G.gn[1], (cuuint64_t)G.gn[2], NV};
+  const cuuint64_t strides[3] = {(cuuint64_t)G.sy * 8, (cuuint64_t)G.sz * 8, (cuuint64_t)G.npts * 8};
+  const cuuint32_t box[4] = {GT_BX, GZ_PY, 1, NV};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)u, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int ENS>
+static bool launch_flux_tma(const hd_plan* p, const double* u, dim3 grid, dim3 block, int zseg,
+                            double* partial, cudaStream_t s) {
+  CUtensorMap tm;
+  if (!state_tensor_map(p, u, &tm)) return false;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gradflux_tma_kernel<ENS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(GtSmem)) != cudaSuccess)
+      return false;
+    attr = true;
+  }
+  const double mu = p->phys.mu;
+  const double q_coef = (-mu) / ((p->phys.gamma - 1.0) * p->phys.prandtl);  // viscous.py:107
+  double* vf = (double*)(p->ws + p->off[HD_BUF_VFLUX]);
+  gradflux_tma_kernel<ENS><<<grid, block, sizeof(GtSmem), s>>>(tm, vf, p->geo, mu, q_coef, zseg,
+                                                                p->phys.gamma, partial);
+  return true;
+}
+
+// grid of the z-marching flux kernel: enough z segments for ~4 waves of 2 blocks
+// per SM; returns the segment length
+static int zm_grid(const hd_plan* p, dim3& grid, dim3& block) {
+  const Geo& G = p->geo;
+  const int64_t cols = (int64_t)(G.n[0] / GZ_TX) * (G.n[1] / GZ_TY);
+  int nseg = (int)((p->sm_count * GZ_MINB * GZ_WAVES + cols - 1) / cols);
+  nseg = nseg < 1 ? 1 : (nseg > G.n[2] ? G.n[2] : nseg);
+  const int zseg = (G.n[2] + nseg - 1) / nseg;
+  nseg = (G.n[2] + zseg - 1) / zseg;
+  block = dim3(GZ_TX, GZ_TY, 1);
+  grid = dim3(G.n[0] / GZ_TX, G.n[1] / GZ_TY, nseg);
+  return zseg;
+}
+
+int launch_enstrophy(const hd_plan* p, const double* u, double* out, cudaStream_t s) {
+  const Geo& G = p->geo;
+  double* partial = (double*)(p->ws + p->off[HD_BUF_ENS]);
+  if (G.n[0] % GZ_TX == 0 && G.n[1] % GZ_TY == 0 && p->opt[HD_OPT_FLUX_ZMARCH]) {
+    // the flux kernel's z march without the flux fields: the state read once
+    dim3 grid, block;
+    const int zseg = zm_grid(p, grid, block);
+    const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
+    if (nblk <= ens_capacity(p->geom)) {
+      if (!p->opt[HD_OPT_FLUX_TMA] || !launch_flux_tma<2>(p, u, grid, block, zseg, partial, s))
+        gradflux_zm_kernel<false, true, 2><<<grid, block, 0, s>>>(u, nullptr, G, 0.0, 0.0, zseg,
+                                                                  p->phys.gamma, partial);
+      sum_finish_kernel<<<1, 32, 0, s>>>(partial, (int)nblk, out);
+      hd::count_launches(2);
+      return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+    }
+  }
+  const int64_t rows = (int64_t)G.n[1] * G.n[2];
+  int blocks = (int)((rows + ENS_THREADS / 32 - 1) / (ENS_THREADS / 32));
+  if (blocks > ENS_BLOCKS_MAX) blocks = ENS_BLOCKS_MAX;
+  enstrophy_kernel<<<blocks, ENS_THREADS, 0, s>>>(u, G, partial);
+  sum_finish_kernel<<<1, 32, 0, s>>>(partial, blocks, out);
+  hd::count_launches(2);
+  return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+}
 
 int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s, double* ens_out,
                     int* ens_folded) {
@@ -464,33 +759,40 @@ int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s, double* e
   const double mu = p->phys.mu;
   const double q_coef = (-mu) / ((p->phys.gamma - 1.0) * p->phys.prandtl);  // viscous.py:107
   if (G.n[0] % GZ_TX == 0 && G.n[1] % GZ_TY == 0 && p->opt[HD_OPT_FLUX_ZMARCH]) {
-    // z segments: enough blocks for ~4 waves of 2 blocks per SM
-    const int64_t cols = (int64_t)(G.n[0] / GZ_TX) * (G.n[1] / GZ_TY);
-    int nseg = (int)((p->sm_count * GZ_MINB * GZ_WAVES + cols - 1) / cols);
-    nseg = nseg < 1 ? 1 : (nseg > G.n[2] ? G.n[2] : nseg);
-    const int zseg = (G.n[2] + nseg - 1) / nseg;
-    nseg = (G.n[2] + zseg - 1) / zseg;
-    dim3 block(GZ_TX, GZ_TY, 1), grid(G.n[0] / GZ_TX, G.n[1] / GZ_TY, nseg);
+    dim3 grid, block;
+    const int zseg = zm_grid(p, grid, block);
     const double gamma = p->phys.gamma;
     const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
     double* ep = (double*)(p->ws + p->off[HD_BUF_ENS]);
     const bool ens = ens_out && nblk <= ens_capacity(p->geom);
+    // fast mode from the state: the TMA-fed kernel when the state maps to a tensor
+    if (!exact && u && p->opt[HD_OPT_FLUX_TMA] &&
+        (ens ? launch_flux_tma<1>(p, u, grid, block, zseg, ep, s)
+             : launch_flux_tma<0>(p, u, grid, block, zseg, ep, s))) {
+      if (ens) {
+        sum_finish_kernel<<<1, 32, 0, s>>>(ep, (int)nblk, ens_out);
+        hd::count_launches(1);
+        if (ens_folded) *ens_folded = 1;
+      }
+      hd::count_launches(1);
+      return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+    }
     if (ens) {
       if (exact)
-        gradflux_zm_kernel<true, false, true><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
+        gradflux_zm_kernel<true, false, 1><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
       else if (u)
-        gradflux_zm_kernel<false, true, true><<<grid, block, 0, s>>>(u, vf, G, mu, q_coef, zseg, gamma, ep);
+        gradflux_zm_kernel<false, true, 1><<<grid, block, 0, s>>>(u, vf, G, mu, q_coef, zseg, gamma, ep);
       else
-        gradflux_zm_kernel<false, false, true><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
+        gradflux_zm_kernel<false, false, 1><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
       sum_finish_kernel<<<1, 32, 0, s>>>(ep, (int)nblk, ens_out);
       hd::count_launches(1);
       if (ens_folded) *ens_folded = 1;
     } else if (exact) {
-      gradflux_zm_kernel<true, false, false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
+      gradflux_zm_kernel<true, false, 0><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
     } else if (u) {
-      gradflux_zm_kernel<false, true, false><<<grid, block, 0, s>>>(u, vf, G, mu, q_coef, zseg, gamma, ep);
+      gradflux_zm_kernel<false, true, 0><<<grid, block, 0, s>>>(u, vf, G, mu, q_coef, zseg, gamma, ep);
     } else {
-      gradflux_zm_kernel<false, false, false><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
+      gradflux_zm_kernel<false, false, 0><<<grid, block, 0, s>>>(prim, vf, G, mu, q_coef, zseg, gamma, ep);
     }
     hd::count_launches(1);
     return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;

@@ -392,32 +392,35 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   // consecutive threads hold consecutive doubles, so every access is bank-
   // conflict free, and the 45-double window stays out of the register file.
   // Otherwise a register window: point w holds line position c - 2 + w.
-  // The VISC/UPDATE roles append 4 columns: the viscous flux group F_dim
-  // (differentiated along the sweep) at the same positions, so D_dim F_dim
-  // reads each flux value from HBM once.
-  // (y 8.28 -> 8.06 ms, z 9.7 -> 9.25 ms at 512^3 against stencil loads)
+  // The VISC/UPDATE roles keep a second ring: the viscous flux group F_dim
+  // (differentiated along the sweep), so D_dim F_dim reads each flux value from
+  // HBM once (y 8.28 -> 8.06 ms, z 9.7 -> 9.25 ms at 512^3 against stencil loads).
+  // Its values go global -> shared with cp.async, one iteration ahead: loaded
+  // into registers instead, their scoreboard was shared with loads issued late in
+  // the previous iteration and the store into the ring stalled on them (ncu: 20%
+  // of the y sweep's and 24% of the z sweep's warp samples).
   constexpr bool VROLE = ROLE != ROLE_PLAIN;
   constexpr bool UPD = ROLE == ROLE_UPDATE || ROLE == ROLE_UPDATE_DIAG;
   constexpr bool DIAG = ROLE == ROLE_UPDATE_DIAG && !EXACT;
-  constexpr bool FWIN = VROLE;
-  constexpr int RV = FWIN ? 13 : 9;  // values per ring slot
-  __shared__ double ring[SMEM_WINDOW ? 5 * RV * SWEEP_THREADS : 1];
+  constexpr bool FWIN = VROLE && SMEM_WINDOW;
+  constexpr int FS = 6;  // flux ring slots: positions c-3 .. c+2 at iteration c
+  __shared__ double ring[SMEM_WINDOW ? 5 * 9 * SWEEP_THREADS : 1];
+  __shared__ double fring[FWIN ? FS * 4 * SWEEP_THREADS : 1];
   double* const mine = ring + threadIdx.y * 32 + threadIdx.x;
-  auto slot = [&](int m) -> double* { return mine + ((m + 5) % 5) * (RV * SWEEP_THREADS); };
+  double* const fmine = fring + threadIdx.y * 32 + threadIdx.x;
+  auto slot = [&](int m) -> double* { return mine + ((m + 5) % 5) * (9 * SWEEP_THREADS); };
+  auto fslot = [&](int m) -> double* { return fmine + ((m + FS) % FS) * (4 * SWEEP_THREADS); };
   double wu[5][NV], wf[5][NV];
-  // viscous flux window: position p -> slot(p) columns 9..12; F(c+1) enters at
-  // iteration c from fpre (loaded one iteration earlier)
-  const bool fwin = FWIN && SMEM_WINDOW && a.vflux;
-  double fpre[4];
-  auto ffetch = [&](int m) {
+  const bool fwin = FWIN && a.vflux;
+  // flux group at position m -> fslot(m); one cp.async group per position
+  auto fissue = [&](int m) {
+    if (fwin) {
+      double* sp = fslot(m);
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
-      fpre[r] = __ldg(a.vflux + (int64_t)vf_field(DIM, r + 1) * np + base + (int64_t)m * sd);
-  };
-  auto fstore = [&](int m) {
-    double* sp = slot(m) + 9 * SWEEP_THREADS;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) sp[r * SWEEP_THREADS] = fpre[r];
+      for (int r = 0; r < 4; ++r)
+        cp_async8(sp + r * SWEEP_THREADS, a.vflux + (int64_t)vf_field(DIM, r + 1) * np + base + (int64_t)m * sd);
+    }
+    cp_async_commit();
   };
 
   // raw loads are issued one iteration before the point enters the window
@@ -455,13 +458,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
     ingest(c0 - 3 + w, pre, wu[w + 1], wf[w + 1]);
   }
   fetch(c0 + 1, pre);
-  if (fwin) {
-    for (int m = c0 - 3; m < c0; ++m) {
-      ffetch(m);
-      fstore(m);
-    }
-    ffetch(c0);
-  }
+  if constexpr (FWIN)
+    for (int m = c0 - 2; m <= c0; ++m) fissue(m);
 
   double lu[NV], lf[NV];  // left states at c-1/2 (carried)
   // fused diagnostics of the new state (ROLE_UPDATE, last stage)
@@ -481,9 +479,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
     }
     ingest(c + 2, pre, wu[4], wf[4]);
     if (c < c1) fetch(c + 3, pre);
-    if (fwin) {
-      fstore(c + 1);
-      if (c < c1) ffetch(c + 2);
+    if constexpr (FWIN) {
+      if (c < c1) fissue(c + 2);
+      else cp_async_commit();  // keep one group per iteration
     }
     const bool wr = c > c0;
     // y sweep: pull the next cell's D_x stencil lines (x group) into L1 a window
@@ -553,10 +551,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
           // then D_dim F_dim from the window, positions c-3 .. c+1
           if constexpr (ROLE == ROLE_VISC)
             add_viscous_divergence<EXACT>(a.vflux, G, base + (int64_t)(c - 1) * sd, 1, val);
-          const double* m2 = slot(c - 3) + 9 * SWEEP_THREADS;
-          const double* m1 = slot(c - 2) + 9 * SWEEP_THREADS;
-          const double* p1 = slot(c) + 9 * SWEEP_THREADS;
-          const double* p2 = slot(c + 1) + 9 * SWEEP_THREADS;
+          cp_async_wait<1>();  // position c+1 landed (c+2 may be in flight)
+          const double* m2 = fslot(c - 3);
+          const double* m1 = fslot(c - 2);
+          const double* p1 = fslot(c);
+          const double* p2 = fslot(c + 1);
           const double coef = 1.0 / (12.0 * G.h[DIM]);
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
@@ -620,19 +619,25 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
 // plain kernel's per-lane loads and stores touch 32 different rows (one sector
 // per lane: partial-sector writes, L1 thrash).  Here the warp moves 4-point
 // chunks of all 32 rows with cp.async (lane l copies row 8i + l/4, position
-// l%4: four full 32-byte sectors per instruction), double-buffered one chunk
-// ahead, and its increments go out the same way through a staging tile.
+// l%4: four full 32-byte sectors per instruction), in a ring of XB buffers
+// filled XB-1 chunks ahead, and its increments go out the same way through a
+// staging tile.
 // ---------------------------------------------------------------------------
 // Chunks of XC = 4 positions per row; staging tiles have row pitch XC + 1
 // doubles (odd: conflict-free 64-bit access).  Chunks of 2 with a shared-memory
 // window ring measured slower at 512^3 (149-165 vs 141 ms/step).
 constexpr int XC = 4;
 constexpr int XS_PAD = XC + 1;
+// Staging ring depth: with 2 buffers (one chunk = 4 cells ahead) the chunk waits
+// are ~23% of the x sweep's warp samples (ncu, 256^3), yet 3 buffers (51 KB of
+// dynamic shared memory per block, same 4 blocks/SM) measured slower: 8.5 -> 10.3
+// ms at 512^3
+constexpr int XB = 2;
 
 template <bool EXACT, int PW>
 __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_staged_kernel(const SweepArgs a) {
   constexpr int WARPS = SWEEP_THREADS / 32;
-  __shared__ double xin[WARPS][2][NV][32 * XS_PAD];
+  __shared__ double xin[WARPS][XB][NV][32 * XS_PAD];
   __shared__ double xout[WARPS][NV][32 * XS_PAD];
   const Geo& G = a.geo;
   const int lane = threadIdx.x, w = threadIdx.y;
@@ -655,7 +660,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
   // copies row (32/XC) i + l/XC, position l % XC (consecutive lanes: consecutive x)
   constexpr int RPI = 32 / XC;  // rows per copy instruction
   auto issue = [&](int t) {
-    const int buf = t & 1;
+    const int buf = t % XB;
     const int xo = lane % XC;
     const int p = p0 + XC * t + xo;
     if (p <= c1 + 2) {
@@ -671,7 +676,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
   };
   auto take = [&](int p, double (&uu)[NV], double (&ff)[NV]) {
     const int q = p - p0;
-    const double* s = &xin[w][(q / XC) & 1][0][lane * XS_PAD + (q % XC)];
+    const double* s = &xin[w][(q / XC) % XB][0][lane * XS_PAD + (q % XC)];
 #pragma unroll
     for (int v = 0; v < NV; ++v) uu[v] = s[v * 32 * XS_PAD];
     double inv, pv[4];
@@ -705,15 +710,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
 
   double wu[5][NV], wf[5][NV];
   // Entering chunk t (its first position is consumed): wait for it -- it was
-  // issued when chunk t-1 was entered -- then issue chunk t+1 into the buffer
-  // chunk t-1 has vacated.  Positions p0 .. p0+3 fill the window first.
-  issue(0);
+  // issued when chunk t-XB+1 was entered, later chunks may still be in flight --
+  // then issue chunk t+XB-1 into the buffer chunk t-1 has vacated.  Positions
+  // p0 .. p0+3 fill the window first.
+#pragma unroll
+  for (int t = 0; t < XB - 1; ++t) issue(t);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     if (q % XC == 0) {
-      cp_async_wait<0>();
+      cp_async_wait<XB - 2>();
       __syncwarp();
-      issue(q / XC + 1);
+      issue(q / XC + XB - 1);
     }
     take(p0 + q, wu[q + 1], wf[q + 1]);
   }
@@ -722,9 +729,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
   for (int c = c0 - 1; c <= c1; ++c) {
     const int p = c + 2;
     if ((p - p0) % XC == 0) {
-      cp_async_wait<0>();
+      cp_async_wait<XB - 2>();
       __syncwarp();
-      issue((p - p0) / XC + 1);
+      issue((p - p0) / XC + XB - 1);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -823,10 +830,9 @@ int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int ac
     constexpr int BY = SWEEP_THREADS / 32;
     const Geo& G = p->geo;
     dim3 block(32, BY, 1), grid(G.n[1] / 32, (G.n[2] + BY - 1) / BY, nseg);
-    if (exact && a.ph.power == 2) sweep_x_staged_kernel<true, 2><<<grid, block, 0, s>>>(a);
-    else if (exact) sweep_x_staged_kernel<true, 0><<<grid, block, 0, s>>>(a);
-    else if (a.ph.power == 2) sweep_x_staged_kernel<false, 2><<<grid, block, 0, s>>>(a);
-    else sweep_x_staged_kernel<false, 0><<<grid, block, 0, s>>>(a);
+    auto kern = exact ? (a.ph.power == 2 ? sweep_x_staged_kernel<true, 2> : sweep_x_staged_kernel<true, 0>)
+                      : (a.ph.power == 2 ? sweep_x_staged_kernel<false, 2> : sweep_x_staged_kernel<false, 0>);
+    kern<<<grid, block, 0, s>>>(a);
     hd::count_launches(1);
     return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
   }

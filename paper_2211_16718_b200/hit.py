@@ -11,7 +11,16 @@ shell mask -> solenoidal projection -> exact per-shell rescale -> inverse FFT):
   tests/golden/traj32.json ``ic_sha256``);
 * ``backend="torch"`` -- the same algorithm in HBM with cuFFT and the torch
   Philox stream: statistically identical, not bit-identical; used for grids
-  whose host synthesis would need tens of GB (512^3, 1024^3).
+  whose host synthesis would need tens of GB (512^3);
+* :func:`synthesize_velocity_slab` / :func:`make_initial_condition_slab` --
+  the same algorithm decomposed over the ranks of a z-slab run (1024^3, where
+  neither one host nor one GPU can hold the global transform next to the
+  solver): every mode comes from a counter-based generator keyed by its
+  global wavevector, so a rank draws any mode -- and its conjugate partner --
+  without communication; the shell energies are summed over ranks before the
+  exact per-shell rescale; the inverse FFT runs over (kz, kx) on ky slabs,
+  one all-to-all, then over ky on the z slabs the solver owns.  The field is
+  the same for every rank count up to FFT round-off.
 """
 
 from __future__ import annotations
@@ -143,6 +152,183 @@ def synthesize_velocity(n: int, params: HitParams, backend: str = "numpy", devic
     if backend == "torch":
         return _synth_torch(n, params, device or torch.device("cuda"))
     raise ValueError(f"backend must be 'numpy' or 'torch', got {backend!r}")
+
+
+# ---- slab-decomposed synthesis ------------------------------------------------------
+def _i64(c: int) -> int:
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+_K_INDEX, _K_SEED, _K_STREAM = _i64(0x9E3779B97F4A7C15), _i64(0xD1B54A32D192ED03), _i64(0x8CB92BA72F3D8DD7)
+_M1, _M2 = _i64(0xBF58476D1CE4E5B9), _i64(0x94D049BB133111EB)
+
+
+def _srl(z: torch.Tensor, s: int) -> torch.Tensor:
+    """Logical right shift of int64 (torch's >> is arithmetic)."""
+    return (z >> s) & ((1 << (64 - s)) - 1)
+
+
+def _uniform(index: torch.Tensor, seed: int, stream: int) -> torch.Tensor:
+    """(0, 1] doubles, a pure function of (index, seed, stream): the splitmix64
+    finaliser over a Weyl-mixed counter (int64 arithmetic wraps)."""
+    offset = _i64((seed * _K_SEED + (stream + 1) * _K_STREAM) % (1 << 64))  # Python ints: wrap here
+    z = index * _K_INDEX + offset
+    z = (z ^ _srl(z, 30)) * _M1
+    z = (z ^ _srl(z, 27)) * _M2
+    z = z ^ _srl(z, 31)
+    return (_srl(z, 11).to(torch.float64) + 1.0) * (2.0 ** -53)
+
+
+def _mode_draw(n: int, seed: int, comp: int, kz, ky, kx) -> torch.Tensor:
+    """Standard complex normal of velocity component ``comp`` at the integer
+    wavevector indices (kz, ky, kx) in [0, n) (broadcast int64 tensors)."""
+    index = ((comp * n + kz) * n + ky) * n + kx
+    r = torch.sqrt(-2.0 * torch.log(_uniform(index, seed, 0)))
+    theta = (2.0 * math.pi) * _uniform(index, seed, 1)
+    return torch.complex(r * torch.cos(theta), r * torch.sin(theta))
+
+
+def _freq(idx: torch.Tensor, n: int) -> torch.Tensor:
+    """fftfreq(n, 1/n) of integer indices: k for k < n/2, k - n above."""
+    return torch.where(idx < (n + 1) // 2, idx, idx - n).to(torch.float64)
+
+
+def _sum_over_ranks(x: torch.Tensor, group) -> torch.Tensor:
+    """Rank-order sum of a small tensor over the group (deterministic)."""
+    import torch.distributed as dist
+
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return x
+    world = dist.get_world_size(group)
+    parts = [torch.empty_like(x) for _ in range(world)]
+    dist.all_gather(parts, x.contiguous(), group=group)
+    total = parts[0].clone()
+    for part in parts[1:]:
+        total += part
+    return total
+
+
+def synthesize_velocity_slab(n: int, params: HitParams, rank: int = 0, world: int = 1, group=None,
+                             device=None, chunk: int = 32):
+    """The rank's z slab (z in [rank n/world, (rank+1) n/world), all y, x) of the
+    solenoidal HIT velocity (hit.py:93-139's algorithm with a counter-based mode
+    generator); (u, v, w) tensors of shape (n/world, n, n).  Collective over
+    ``group`` (all ranks call it); world = 1 runs it on one device."""
+    if n < 4:
+        raise ConfigError(f"need n >= 4 to hold at least one spectral shell, got {n}")
+    if n % world:
+        raise ConfigError(f"{world} ranks do not divide n = {n}")
+    dev = torch.device(device) if device is not None else (
+        torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else torch.device("cpu"))
+    span = n // world
+    ky_lo = rank * span
+    idx = torch.arange(n, dtype=torch.int64, device=dev)
+    ky_i = idx[ky_lo:ky_lo + span][None, :, None]
+    kx_i = idx[None, None, :]
+    fy, fx = _freq(ky_i, n), _freq(kx_i, n)
+    mirror = lambda i: (n - i) % n  # noqa: E731 - index of the conjugate partner
+    c = torch.empty((3, n, span, n), dtype=torch.complex128, device=dev)
+    raw = np.zeros(n, dtype=np.float64)
+    # modes, Hermitian symmetrisation, shell mask, solenoidal projection and the
+    # shell energies, chunk by chunk along kz (bounded temporaries)
+    for z0 in range(0, n, chunk):
+        kz_i = idx[z0:z0 + chunk][:, None, None]
+        fz = _freq(kz_i, n)
+        k2 = fx * fx + fy * fy + fz * fz
+        shell = torch.floor(torch.sqrt(k2) + 0.5).to(torch.int64)
+        keep = ((shell >= 1) & (shell < n // 2)).to(torch.float64)
+        part = torch.stack([0.5 * (_mode_draw(n, params.seed, a, kz_i, ky_i, kx_i) +
+                                   torch.conj(_mode_draw(n, params.seed, a, mirror(kz_i), mirror(ky_i),
+                                                         mirror(kx_i))))
+                            for a in range(3)]) * keep
+        kdot = (fx * part[0] + fy * part[1] + fz * part[2]) / torch.where(k2 == 0.0, torch.ones_like(k2), k2)
+        part[0] -= fx * kdot
+        part[1] -= fy * kdot
+        part[2] -= fz * kdot
+        energy = 0.5 * (part.real ** 2 + part.imag ** 2).sum(dim=0)
+        # host bincount: sequential, so the sums are reproducible bit for bit
+        raw += np.bincount(shell.expand_as(energy).reshape(-1).cpu().numpy(),
+                           weights=energy.reshape(-1).cpu().numpy(), minlength=n)[:n]
+        c[:, z0:z0 + chunk] = part
+        del part, kdot, energy
+    raw = _sum_over_ranks(torch.from_numpy(raw).to(dev), group).cpu().numpy()
+    scale = torch.from_numpy(_shell_scale(raw, n, params)).to(dev)
+    for z0 in range(0, n, chunk):
+        fz = _freq(idx[z0:z0 + chunk][:, None, None], n)
+        shell = torch.floor(torch.sqrt(fx * fx + fy * fy + fz * fz) + 0.5).to(torch.int64)
+        c[:, z0:z0 + chunk] *= scale[shell]
+    vel = []
+    for a in range(3):
+        # (kz, ky slab, kx) -> (z, ky slab, x), then z slabs to their owners
+        ca = torch.fft.ifft(torch.fft.ifft(c[a], dim=2), dim=0)
+        if world > 1:
+            import torch.distributed as dist
+
+            send = torch.view_as_real(ca).contiguous()  # (P z-blocks x span, span, n, 2)
+            recv = torch.empty_like(send)
+            dist.all_to_all_single(recv, send, group=group)
+            # recv[r] = z block of this rank, ky slab of rank r -> (z, ky, x)
+            ca = torch.view_as_complex(recv.view(world, span, span, n, 2).permute(1, 0, 2, 3, 4)
+                                       .reshape(span, n, n, 2).contiguous())
+        vel.append(torch.fft.ifft(ca, dim=1).real.contiguous())
+        del ca
+    del c
+    return tuple(vel)
+
+
+def compute_spectrum_slab(u, v, w, rank: int = 0, world: int = 1, group=None) -> "SpectrumTable":
+    """compute_spectrum of a field held as z slabs (u, v, w: this rank's
+    (n/world, n, n) tensors): forward FFT over (y, x) on the slab, one
+    all-to-all to ky slabs, FFT over z; shell energies summed over ranks in rank
+    order.  Every rank gets the table.  Collective over ``group``."""
+    span, n = u.shape[0], u.shape[-1]
+    dev = u.device
+    idx = torch.arange(n, dtype=torch.int64, device=dev)
+    fy = _freq(idx[rank * span:(rank + 1) * span][None, :, None], n)
+    fx = _freq(idx[None, None, :], n)
+    fz = _freq(idx[:, None, None], n)
+    shell = torch.floor(torch.sqrt(fx * fx + fy * fy + fz * fz) + 0.5).to(torch.int64)
+    energy = torch.zeros((n, span, n), dtype=torch.float64, device=dev)
+    for comp in (u, v, w):
+        a = torch.fft.fftn(comp, dim=(1, 2))  # (z slab, ky, kx)
+        if world > 1:
+            import torch.distributed as dist
+
+            send = torch.view_as_real(a.reshape(span, world, span, n).permute(1, 0, 2, 3).contiguous())
+            recv = torch.empty_like(send)
+            dist.all_to_all_single(recv, send, group=group)
+            a = torch.view_as_complex(recv.reshape(n, span, n, 2))  # (z, ky slab, kx)
+        a = torch.fft.fft(a, dim=0)
+        energy += a.real ** 2 + a.imag ** 2
+        del a
+    energy /= 2.0 * float(n) ** 6
+    binned = np.bincount(shell.expand_as(energy).reshape(-1).cpu().numpy(),
+                         weights=energy.reshape(-1).cpu().numpy(), minlength=n)[:n]
+    binned = _sum_over_ranks(torch.from_numpy(binned).to(dev), group).cpu().numpy()
+    return SpectrumTable(np.arange(n, dtype=np.int64), binned, n)
+
+
+def make_initial_condition_slab(spec: GridSpec, params: HitParams, layout, group=None,
+                                gamma: float = 1.4, device=None) -> FieldSet:
+    """The block of ``layout`` (a z-slab RankLayout of ``spec``, decomp.decompose)
+    of the HIT initial condition, synthesised across the group's ranks
+    (:func:`synthesize_velocity_slab`); rho0, p0 = rho0/gamma, ghosts zero."""
+    n = spec.n[0]
+    if spec.n[1] != n or spec.n[2] != n:
+        raise ConfigError(f"initial condition needs a cubic grid, got n={spec.n}")
+    if tuple(layout.dims[:2]) != (1, 1):
+        raise ConfigError(f"slab synthesis needs z slabs (1, 1, P), got dims {layout.dims}")
+    world = layout.dims[2]
+    u, v, w = synthesize_velocity_slab(n, params, layout.coords[2], world, group, device)
+    rho0, p0 = params.rho0, params.rho0 / gamma
+    fields = FieldSet.zeros(layout.spec, Layout.COMPONENT_CONTIGUOUS, device=u.device)
+    it = fields.interior()
+    it[0] = rho0
+    it[1] = rho0 * u
+    it[2] = rho0 * v
+    it[3] = rho0 * w
+    it[4] = p0 / (gamma - 1.0) + 0.5 * rho0 * (u * u + v * v + w * w)
+    return fields
 
 
 @dataclass

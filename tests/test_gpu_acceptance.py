@@ -175,3 +175,33 @@ def test_fast_mode_ke_curve_tracks_exact(hd):
     b = fa.fields.interior().reshape(5, -1)
     rel = ((b - a).norm(dim=1) / a.norm(dim=1)).cpu().numpy()
     assert np.all(rel <= 1e-10), rel
+
+
+@pytest.mark.parametrize("n", [(32, 32, 32), (64, 40, 24)])
+def test_flux_kernel_variants_agree(hd, n):
+    """The TMA-fed flux kernel (HD_OPT_FLUX_TMA), the register-prefetch z-marching
+    kernel and the pointwise kernel compute the same viscous fluxes (fast mode: the
+    compiler may contract their FMAs differently), so 2 fast-mode RK4 steps
+    (enstrophy folded into the first flux kernel) agree to round-off."""
+    spec = hd.GridSpec(n)
+    rng = np.random.default_rng(9)
+    shape = spec.interior_shape
+    rho = torch.from_numpy(0.8 + 0.4 * rng.random(shape)).cuda()
+    vel = [torch.from_numpy(0.3 * rng.standard_normal(shape)).cuda() for _ in range(3)]
+    p = torch.from_numpy(0.8 + 0.4 * rng.random(shape)).cuda()
+    fs = _from_prims(hd, spec, rho, *vel, p)
+    gas = hd.GasModel(mu=0.02)
+    outs = []
+    for tma, zmarch in ((1, 1), (0, 1), (0, 0)):
+        hd.release_plans()
+        plan = hd.get_plan(spec, gas, mode="fast")
+        plan.set_option(hd._lib.HD_OPT_FLUX_TMA, tma)
+        plan.set_option(hd._lib.HD_OPT_FLUX_ZMARCH, zmarch)
+        res = hd.advance(fs, gas, hd.TimeParams(scheme="rk4", cfl=0.3, max_steps=2), mode="fast")
+        outs.append((res.fields.interior().cpu().numpy(), [r.enstrophy for r in res.records]))
+    hd.release_plans()
+    for other in (outs[1][0], outs[2][0]):
+        rel = np.sqrt(((other - outs[0][0]) ** 2).reshape(5, -1).sum(1) /
+                      (outs[0][0] ** 2).reshape(5, -1).sum(1))
+        assert np.all(rel <= 1e-14), rel
+    assert np.allclose(outs[0][1], outs[1][1], rtol=1e-13) and np.allclose(outs[0][1], outs[2][1], rtol=1e-13)

@@ -33,7 +33,13 @@ def test_torch_ic_shells_match_target(hd, n):
     u, v, w = hd.synthesize_velocity(n, P, "torch")
     table = hd.compute_spectrum(u, v, w)
     want = hd.target_spectrum(np.arange(1, n // 2, dtype=np.float64))
-    np.testing.assert_allclose(table.energy[1:n // 2], want, rtol=1e-12, atol=0.0)
+    got = table.energy[1:n // 2]
+    # shells whose target lies well above the transform's absolute round-off
+    # (~3e-26 at n <= 512; at n = 32 that is every shell, as in the reference
+    # test) match to 1e-12; the far tail only to that round-off
+    above = want > 1e-13
+    np.testing.assert_allclose(got[above], want[above], rtol=1e-12, atol=0.0)
+    assert np.all(np.abs(got[~above] - want[~above]) < 1e-24)
     assert table.energy[0] < 1e-30
     assert np.all(table.energy[n // 2:] < 1e-20)
 
