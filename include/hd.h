@@ -62,7 +62,8 @@ extern "C" {
 #define HD_OPT_X_STAGED 1      /* 1 (default): cp.async-staged x sweep when n_y % 32 == 0; 0: plain */
 #define HD_OPT_FLUX_ZMARCH 2   /* 1 (default): z-marching viscous flux kernel when the tiles fit; 0: pointwise */
 #define HD_OPT_FLUX_TMA 3      /* 1 (default): fast-mode flux kernel fed by TMA when the state maps to a tensor */
-#define HD_OPT_N 4
+#define HD_OPT_SWEEP_WAVES 4   /* automatic sweep segments: lines x segments >= this many waves of 256 threads/SM (default 6) */
+#define HD_OPT_N 5
 
 /* workspace buffers (hd_plan_buffer) */
 #define HD_BUF_STAGE 0 /* 10 fields: RK stage states, ping-pong halves (stage s writes half s%2) */
@@ -145,6 +146,17 @@ int hd_fill_ghosts(hd_plan* plan, double* fields, int nfields, void* stream);
  * accumulate=1: inc -= dF/dx; accumulate=0: inc = 0 - dF/dx (interior only). */
 int hd_hyper_sweep(hd_plan* plan, int dim, const double* u, double* inc, int accumulate,
                    void* stream);
+
+/* kernels.py:68-73 hyper_sweep with the reference's exact argument list, on device
+ * buffers: accumulates -dF/dx of dimension `dim` into inc for the slab of lines
+ * [a_lo, a_hi) x [0, nb) (line origin base0 + ia*sa + ib*sb, stride sd, nd cells),
+ * reconstructing the caller's flux array f (upwind.py:116-127).  Exact IEEE
+ * arithmetic, bitwise equal to the numba kernel: the one-for-one replacement
+ * inside the reference's run_slabs loop (upwind.py:185-212). */
+int hd_hyper_sweep_lines(const double* u, const double* f, double* inc, int64_t npts, int64_t base0,
+                         int64_t sd, int64_t sa, int64_t sb, int64_t nd, int64_t nb, int64_t a_lo,
+                         int64_t a_hi, int dim, double inv_dx, double gamma, double eps, int power,
+                         double delta, void* stream);
 
 /* upwind.py:163-213 hyperbolic_rhs: x, y, z sweeps; also latches positivity. */
 int hd_hyperbolic_rhs(hd_plan* plan, const double* u, double* inc, int accumulate, void* stream);

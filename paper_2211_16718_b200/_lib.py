@@ -23,7 +23,7 @@ HD_MODE_EXACT = 1
 HD_SCHEME_RK3 = 3
 HD_SCHEME_RK4 = 4
 HD_PART_LOCAL, HD_PART_HALO, HD_PART_MID, HD_PART_UPDATE, HD_PART_ALL = 1, 2, 4, 8, 15
-HD_OPT_SEGMENTS, HD_OPT_X_STAGED, HD_OPT_FLUX_ZMARCH, HD_OPT_FLUX_TMA = 0, 1, 2, 3
+HD_OPT_SEGMENTS, HD_OPT_X_STAGED, HD_OPT_FLUX_ZMARCH, HD_OPT_FLUX_TMA, HD_OPT_SWEEP_WAVES = 0, 1, 2, 3, 4
 (HD_BUF_STAGE, HD_BUF_ACC, HD_BUF_INC, HD_BUF_PRIM, HD_BUF_VFLUX, HD_BUF_RED, HD_BUF_CTX,
  HD_BUF_ERR, HD_BUF_STATE, HD_BUF_SYNC, HD_BUF_FRED, HD_BUF_ENS) = range(12)
 HD_PEER_STATE, HD_PEER_VFLUX = 0, 1
@@ -43,7 +43,7 @@ EXPORTS = (
     "hd_timer_read", "hd_ipc_handle", "hd_ipc_open", "hd_ipc_close", "hd_peer_attach", "hd_peer_attach3", "hd_peer_signal",
     "hd_peer_wait", "hd_peer_timed_out", "hd_stage_buffer", "hd_rk4_step", "hd_max_signal",
     "hd_totals", "hd_error_flags", "hd_halo_exchange", "hd_viscous_fluxes", "hd_viscous_divergence",
-    "hd_arm_reduce", "hd_enstrophy", "hd_arm_enstrophy",
+    "hd_arm_reduce", "hd_enstrophy", "hd_arm_enstrophy", "hd_hyper_sweep_lines",
 )
 # hd_timer_read kinds (HD_TK_*)
 TIMER_KINDS = ("sweep_x", "sweep_y", "sweep_z", "gradflux", "prims", "divergence", "reduce")
@@ -125,6 +125,7 @@ def load(require_cuda: bool = False):
             "hd_rk4_step": ([P, P, P, P], i32),
             "hd_arm_reduce": ([P, P, i64], i32),
             "hd_enstrophy": ([P, P, P, P], i32),
+            "hd_hyper_sweep_lines": ([P, P, P] + [i64] * 9 + [i32, f64, f64, f64, i32, f64, P], i32),
             "hd_arm_enstrophy": ([P, P], i32),
             "hd_viscous_fluxes": ([P, P, P], i32),
             "hd_viscous_divergence": ([P, P, P], i32),

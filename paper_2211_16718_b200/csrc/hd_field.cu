@@ -461,16 +461,23 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_zm_kernel(
 // register z queue, the halo ring of plane k into the primitive tile) and
 // compute.  One barrier per plane, as before: it also retires the raw slot.
 // ---------------------------------------------------------------------------
-constexpr int GT_S = 4;
-constexpr int GT_BX = GZ_PX + 2;      // box width: x - 3 .. x + 34 of the tile, 304 B rows
-constexpr int GT_BOX = NV * GZ_PY * GT_BX;          // doubles per box (18,240 B)
-constexpr int GT_SLOT = (GT_BOX + 15) / 16 * 16;    // slots 128-byte aligned (TMA destination)
-struct GtSmem {
-  double raw[GT_S][GT_SLOT];           // 73,216 B
-  double tile[2][4][GZ_PY][GZ_PX];     // 27,648 B (primitive planes, double-buffered)
-  unsigned long long full[GT_S];       // mbarriers
+constexpr int GT_BX = GZ_PX + 2;  // box width: x - 3 .. x + 34 of the tile, 304 B rows
+// Tile shape and ring depth of the TMA kernel: 32 x 8 tiles, a 4-plane ring, 2
+// blocks/SM (3.64 ms per launch at 512^3 against 3.93 for the register-prefetch
+// kernel).  32 x 16 tiles with a 5-plane ring at 1 block of 16 warps/SM (more
+// bytes in flight, 17% less halo) measured 3.91 ms (tools/gpu/flux_probe.py).
+template <int TY_, int S_> struct GtCfg {
+  static constexpr int TY = TY_, S = S_, PY = TY + 2 * GZ_H;
+  static constexpr int MINB = TY <= 8 ? 2 : 1;
+  static constexpr int BOX = NV * PY * GT_BX;          // doubles per box
+  static constexpr int SLOT = (BOX + 15) / 16 * 16;    // slots 128-byte aligned (TMA destination)
+  struct Smem {
+    double raw[S][SLOT];
+    double tile[2][4][PY][GZ_PX];  // primitive planes, double-buffered
+    unsigned long long full[S];    // mbarriers
+  };
 };
-constexpr unsigned GT_BOX_BYTES = GT_BOX * 8;
+using GtSmall = GtCfg<8, 4>;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -500,21 +507,23 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, in
       : "memory");
 }
 
-template <int ENS>
-__global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_tma_kernel(
+template <int ENS, class C>
+__global__ void __launch_bounds__(GZ_TX * C::TY, C::MINB) gradflux_tma_kernel(
     const __grid_constant__ CUtensorMap tm, double* __restrict__ vf, Geo G, double mu, double q_coef,
     int zseg, double gamma, double* ens_partial) {
+  constexpr int TY = C::TY, PY = C::PY, GT_S = C::S;
+  constexpr unsigned BOX_BYTES = C::BOX * 8;
   extern __shared__ __align__(128) unsigned char gt_smem[];
-  GtSmem& S = *reinterpret_cast<GtSmem*>(gt_smem);
+  typename C::Smem& S = *reinterpret_cast<typename C::Smem*>(gt_smem);
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * GZ_TX + tx;
-  const int i = blockIdx.x * GZ_TX + tx, j = blockIdx.y * GZ_TY + ty;
+  const int i = blockIdx.x * GZ_TX + tx, j = blockIdx.y * TY + ty;
   const int k0 = blockIdx.z * zseg;
   const int k1 = min(k0 + zseg, G.n[2]);
   const int g = G.g;
   const int p0 = k0 - 2, plast = k1 + 1;  // planes the z stencils touch
   // box origin (ghosted coordinates): x one column left of the halo, even, so the
   // row start is 16-byte aligned (n_x % 32 == 0, g = 3 -> 32 bx + g - 3)
-  const int bx = blockIdx.x * GZ_TX - GZ_H - 1 + g, by = blockIdx.y * GZ_TY - GZ_H + g;
+  const int bx = blockIdx.x * GZ_TX - GZ_H - 1 + g, by = blockIdx.y * TY - GZ_H + g;
   double coef[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) coef[d] = 1.0 / (12.0 * G.h[d]);
@@ -527,7 +536,7 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_tma_kernel(
   __syncthreads();
   auto issue = [&](int p) {  // thread 0
     const int s = (p - p0) % GT_S;
-    mbar_expect_tx(&S.full[s], GT_BOX_BYTES);
+    mbar_expect_tx(&S.full[s], BOX_BYTES);
     tma_load_4d(&S.raw[s][0], &tm, bx, by, p + g, 0, &S.full[s]);
   };
   auto wait_plane = [&](int p) {
@@ -538,7 +547,7 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_tma_kernel(
     const int s = (p - p0) % GT_S;
     double c[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) c[v] = S.raw[s][(v * GZ_PY + py) * GT_BX + px + 1];
+    for (int v = 0; v < NV; ++v) c[v] = S.raw[s][(v * PY + py) * GT_BX + px + 1];
     prims_of(c, gamma, gm1, pv);
   };
   if (tid == 0)
@@ -557,24 +566,24 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_tma_kernel(
   // halo ring of the primitive tile (minus the never-read corners): <= 1 point per thread
   const int r = tid;
   int px = 0, py = 0;
-  bool has_ring = r < GZ_PX * GZ_PY - GZ_TX * GZ_TY;
+  bool has_ring = r < GZ_PX * PY - GZ_TX * TY;
   if (has_ring) {
     if (r < 2 * GZ_H * GZ_PX) {
       py = r / GZ_PX;
       px = r % GZ_PX;
-      if (py >= GZ_H) py += GZ_TY;
+      if (py >= GZ_H) py += TY;
     } else {
       const int s = r - 2 * GZ_H * GZ_PX;
       py = GZ_H + s / (2 * GZ_H);
       px = s % (2 * GZ_H);
       if (px >= GZ_H) px += GZ_TX;
     }
-    has_ring = !((px < GZ_H || px >= GZ_H + GZ_TX) && (py < GZ_H || py >= GZ_H + GZ_TY));
+    has_ring = !((px < GZ_H || px >= GZ_H + GZ_TX) && (py < GZ_H || py >= GZ_H + TY));
   }
   __syncthreads();  // planes k0-2 and k0-1 were needed for their centres only
   if (tid == 0) {
-    if (k0 + 2 <= plast) issue(k0 + 2);
-    if (k0 + 3 <= plast) issue(k0 + 3);
+    if (k0 + GT_S - 2 <= plast) issue(k0 + GT_S - 2);
+    if (k0 + GT_S - 1 <= plast) issue(k0 + GT_S - 1);
   }
   const int pm = periodic_mask(G);
   const int64_t np = G.npts, sz = G.sz;
@@ -596,11 +605,11 @@ __global__ void __launch_bounds__(GZ_TX * GZ_TY, GZ_MINB) gradflux_tma_kernel(
       if (has_ring) S.tile[b][f][py][px] = pr[f];
     }
     __syncthreads();
-    // every thread is done with raw plane k: its slot takes plane k + 4
-    if (tid == 0 && k + 4 <= plast) issue(k + 4);
+    // every thread is done with raw plane k: its slot takes plane k + S
+    if (tid == 0 && k + GT_S <= plast) issue(k + GT_S);
     double gr[3][3], gT[3];
     const int cx = tx + GZ_H, cy = ty + GZ_H;
-    double (*tl)[GZ_PY][GZ_PX] = S.tile[b];
+    double (*tl)[PY][GZ_PX] = S.tile[b];
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       const double gx = cd4v<false>(tl[f][cy][cx - 2], tl[f][cy][cx - 1], tl[f][cy][cx + 1],
@@ -674,7 +683,7 @@ static EncodeTiledFn encode_tiled_fn() {
 // The state u as a 4D tensor (x, y, z, variable) for TMA; false when the
 // geometry or alignment does not allow it (odd extents: 8-byte rows are not
 // 16-byte strides)
-static bool state_tensor_map(const hd_plan* p, const double* u, CUtensorMap* tm) {
+static bool state_tensor_map(const hd_plan* p, const double* u, int py, CUtensorMap* tm) {
   const Geo& G = p->geo;
   EncodeTiledFn enc = encode_tiled_fn();
   // 16-byte aligned rows and box origins: even ghosted x extent, g odd (origin
@@ -682,45 +691,63 @@ static bool state_tensor_map(const hd_plan* p, const double* u, CUtensorMap* tm)
   if (!enc || (G.gn[0] % 2) || ((G.g - 3) % 2) || ((uintptr_t)u % 16)) return false;
   const cuuint64_t dims[4] = {(cuuint64_t)G.gn[0], (cuuint64_t)G.gn[1], (cuuint64_t)G.gn[2], NV};
   const cuuint64_t strides[3] = {(cuuint64_t)G.sy * 8, (cuuint64_t)G.sz * 8, (cuuint64_t)G.npts * 8};
-  const cuuint32_t box[4] = {GT_BX, GZ_PY, 1, NV};
+  const cuuint32_t box[4] = {GT_BX, (cuuint32_t)py, 1, NV};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)u, dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int ENS>
-static bool launch_flux_tma(const hd_plan* p, const double* u, dim3 grid, dim3 block, int zseg,
-                            double* partial, cudaStream_t s) {
+template <int ENS, class C>
+static bool launch_flux_tma_cfg(const hd_plan* p, const double* u, dim3 grid, dim3 block, int zseg,
+                                double* partial, cudaStream_t s) {
   CUtensorMap tm;
-  if (!state_tensor_map(p, u, &tm)) return false;
+  if (!state_tensor_map(p, u, C::PY, &tm)) return false;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(gradflux_tma_kernel<ENS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(GtSmem)) != cudaSuccess)
+    if (cudaFuncSetAttribute(gradflux_tma_kernel<ENS, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(typename C::Smem)) != cudaSuccess)
       return false;
     attr = true;
   }
   const double mu = p->phys.mu;
   const double q_coef = (-mu) / ((p->phys.gamma - 1.0) * p->phys.prandtl);  // viscous.py:107
   double* vf = (double*)(p->ws + p->off[HD_BUF_VFLUX]);
-  gradflux_tma_kernel<ENS><<<grid, block, sizeof(GtSmem), s>>>(tm, vf, p->geo, mu, q_coef, zseg,
-                                                                p->phys.gamma, partial);
+  gradflux_tma_kernel<ENS, C><<<grid, block, sizeof(typename C::Smem), s>>>(tm, vf, p->geo, mu, q_coef,
+                                                                            zseg, p->phys.gamma, partial);
   return true;
+}
+
+static int zm_grid_ty(const hd_plan* p, int ty, int minb, dim3& grid, dim3& block);
+
+// the TMA flux kernel on its own grid (*nblk: the ENS partial count); false when
+// the state cannot be mapped (the caller falls back to the register-prefetch kernel)
+template <int ENS>
+static bool launch_flux_tma(const hd_plan* p, const double* u, double* partial, int64_t* nblk,
+                            cudaStream_t s) {
+  dim3 grid, block;
+  const int zseg = zm_grid_ty(p, GtSmall::TY, GtSmall::MINB, grid, block);
+  *nblk = (int64_t)grid.x * grid.y * grid.z;
+  if (ENS && *nblk > ens_capacity(p->geom)) return false;
+  return launch_flux_tma_cfg<ENS, GtSmall>(p, u, grid, block, zseg, partial, s);
 }
 
 // grid of the z-marching flux kernel: enough z segments for ~4 waves of 2 blocks
 // per SM; returns the segment length
-static int zm_grid(const hd_plan* p, dim3& grid, dim3& block) {
+static int zm_grid_ty(const hd_plan* p, int ty, int minb, dim3& grid, dim3& block) {
   const Geo& G = p->geo;
-  const int64_t cols = (int64_t)(G.n[0] / GZ_TX) * (G.n[1] / GZ_TY);
-  int nseg = (int)((p->sm_count * GZ_MINB * GZ_WAVES + cols - 1) / cols);
+  const int64_t cols = (int64_t)(G.n[0] / GZ_TX) * (G.n[1] / ty);
+  int nseg = (int)((p->sm_count * minb * GZ_WAVES + cols - 1) / cols);
   nseg = nseg < 1 ? 1 : (nseg > G.n[2] ? G.n[2] : nseg);
   const int zseg = (G.n[2] + nseg - 1) / nseg;
   nseg = (G.n[2] + zseg - 1) / zseg;
-  block = dim3(GZ_TX, GZ_TY, 1);
-  grid = dim3(G.n[0] / GZ_TX, G.n[1] / GZ_TY, nseg);
+  block = dim3(GZ_TX, ty, 1);
+  grid = dim3(G.n[0] / GZ_TX, G.n[1] / ty, nseg);
   return zseg;
+}
+
+static int zm_grid(const hd_plan* p, dim3& grid, dim3& block) {
+  return zm_grid_ty(p, GZ_TY, GZ_MINB, grid, block);
 }
 
 int launch_enstrophy(const hd_plan* p, const double* u, double* out, cudaStream_t s) {
@@ -731,10 +758,15 @@ int launch_enstrophy(const hd_plan* p, const double* u, double* out, cudaStream_
     dim3 grid, block;
     const int zseg = zm_grid(p, grid, block);
     const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
+    int64_t tb = 0;
+    if (p->opt[HD_OPT_FLUX_TMA] && launch_flux_tma<2>(p, u, partial, &tb, s)) {
+      sum_finish_kernel<<<1, 32, 0, s>>>(partial, (int)tb, out);
+      hd::count_launches(2);
+      return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+    }
     if (nblk <= ens_capacity(p->geom)) {
-      if (!p->opt[HD_OPT_FLUX_TMA] || !launch_flux_tma<2>(p, u, grid, block, zseg, partial, s))
-        gradflux_zm_kernel<false, true, 2><<<grid, block, 0, s>>>(u, nullptr, G, 0.0, 0.0, zseg,
-                                                                  p->phys.gamma, partial);
+      gradflux_zm_kernel<false, true, 2><<<grid, block, 0, s>>>(u, nullptr, G, 0.0, 0.0, zseg,
+                                                                p->phys.gamma, partial);
       sum_finish_kernel<<<1, 32, 0, s>>>(partial, (int)nblk, out);
       hd::count_launches(2);
       return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
@@ -766,11 +798,11 @@ int launch_gradflux(const hd_plan* p, const double* u, cudaStream_t s, double* e
     double* ep = (double*)(p->ws + p->off[HD_BUF_ENS]);
     const bool ens = ens_out && nblk <= ens_capacity(p->geom);
     // fast mode from the state: the TMA-fed kernel when the state maps to a tensor
+    int64_t tb = 0;
     if (!exact && u && p->opt[HD_OPT_FLUX_TMA] &&
-        (ens ? launch_flux_tma<1>(p, u, grid, block, zseg, ep, s)
-             : launch_flux_tma<0>(p, u, grid, block, zseg, ep, s))) {
-      if (ens) {
-        sum_finish_kernel<<<1, 32, 0, s>>>(ep, (int)nblk, ens_out);
+        (ens_out ? launch_flux_tma<1>(p, u, ep, &tb, s) : launch_flux_tma<0>(p, u, ep, &tb, s))) {
+      if (ens_out) {
+        sum_finish_kernel<<<1, 32, 0, s>>>(ep, (int)tb, ens_out);
         hd::count_launches(1);
         if (ens_folded) *ens_folded = 1;
       }

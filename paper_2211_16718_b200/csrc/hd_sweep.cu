@@ -809,7 +809,8 @@ static SweepArgs make_args(const hd_plan* p, int dim, const double* u, double* i
   a.tag = tag;
   // segment length: enough independent lines to fill ~6 waves of 148 SMs x 256 threads
   const int64_t lines = (int64_t)G.n[0] * G.n[1] * G.n[2] / G.n[dim];
-  const int64_t target = (int64_t)p->sm_count * 256 * 6;
+  const int64_t waves = p->opt[HD_OPT_SWEEP_WAVES] > 0 ? p->opt[HD_OPT_SWEEP_WAVES] : 6;
+  const int64_t target = (int64_t)p->sm_count * 256 * waves;
   nseg = (int)((target + lines - 1) / lines);
   if (nseg < 1) nseg = 1;
   if (nseg > G.n[dim] / 8) nseg = G.n[dim] / 8 > 0 ? G.n[dim] / 8 : 1;
@@ -881,4 +882,100 @@ int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, co
   return launch_dim<2, false, ROLE_UPDATE>(p, a, nseg, s);
 }
 
+// ---------------------------------------------------------------------------
+// kernels.py:68-204 hyper_sweep with the reference's own argument list: a slab of
+// lines [a_lo, a_hi) x [0, nb) from base0 with strides (sd, sa, sb), the flux
+// components taken from the caller's array f (upwind.py:116-127 output), exact
+// IEEE arithmetic in the reference order.  One thread per line, one interface at
+// a time -- the compatibility entry for a caller that keeps the reference's
+// run_slabs loop (upwind.py:30-45, 185-212); the fused sweeps above are the
+// fast path.
+// ---------------------------------------------------------------------------
+struct LineArgs {
+  const double* u;
+  const double* f;
+  double* inc;
+  int64_t npts, base0, sd, sa, sb, nd, nb, a_lo, a_hi;
+  double inv_dx, eps;
+  int power;
+  Phys ph;
+};
+
+template <int DIM>
+__global__ void hyper_sweep_lines_kernel(const LineArgs a) {
+  const int64_t line = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nlines = (a.a_hi - a.a_lo) * a.nb;
+  if (line >= nlines) return;
+  const int64_t ia = a.a_lo + line / a.nb, ib = line % a.nb;
+  const int64_t base = a.base0 + ia * a.sa + ib * a.sb;
+  double fprev[NV];
+  for (int64_t m = -1; m < a.nd; ++m) {
+    const int64_t c = base + m * a.sd;
+    double uL[NV], uR[NV], fL[NV], fR[NV], flux[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double* qu = a.u + v * a.npts + c;
+      const double* qf = a.f + v * a.npts + c;
+      const int64_t s = a.sd;
+      uL[v] = recon5_exact(qu[-2 * s], qu[-s], qu[0], qu[s], qu[2 * s], a.eps, a.power);
+      uR[v] = recon5_exact(qu[3 * s], qu[2 * s], qu[s], qu[0], qu[-s], a.eps, a.power);
+      fL[v] = recon5_exact(qf[-2 * s], qf[-s], qf[0], qf[s], qf[2 * s], a.eps, a.power);
+      fR[v] = recon5_exact(qf[3 * s], qf[2 * s], qf[s], qf[0], qf[-s], a.eps, a.power);
+    }
+    roe_flux<DIM, true>(uL, uR, fL, fR, a.ph, flux);
+    if (m >= 0) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double* q = a.inc + v * a.npts + c;
+        *q = xs(*q, xm(xs(flux[v], fprev[v]), a.inv_dx));
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) fprev[v] = flux[v];
+  }
+}
+
 }  // namespace hd
+
+extern "C" int hd_hyper_sweep_lines(const double* u, const double* f, double* inc, int64_t npts,
+                                    int64_t base0, int64_t sd, int64_t sa, int64_t sb, int64_t nd,
+                                    int64_t nb, int64_t a_lo, int64_t a_hi, int dim, double inv_dx,
+                                    double gamma, double eps, int power, double delta, void* stream) {
+  using namespace hd;
+  if (!u || !f || !inc || dim < 0 || dim > 2 || npts < 1 || nd < 0 || nb < 0 || a_hi < a_lo || power < 1)
+    return HD_E_ARG;
+  const int64_t nlines = (a_hi - a_lo) * nb;
+  if (nlines == 0 || nd == 0) return HD_OK;
+  LineArgs a;
+  a.u = u;
+  a.f = f;
+  a.inc = inc;
+  a.npts = npts;
+  a.base0 = base0;
+  a.sd = sd;
+  a.sa = sa;
+  a.sb = sb;
+  a.nd = nd;
+  a.nb = nb;
+  a.a_lo = a_lo;
+  a.a_hi = a_hi;
+  a.inv_dx = inv_dx;
+  a.eps = eps;
+  a.power = power;
+  a.ph.gamma = gamma;
+  a.ph.gm1 = gamma - 1.0;  // kernels.py:84
+  a.ph.delta = delta;
+  a.ph.eps = eps;
+  a.ph.power = power;
+  a.ph.prandtl = 0.0;
+  a.ph.mu = 0.0;
+  const int threads = 128;
+  const unsigned blocks = (unsigned)((nlines + threads - 1) / threads);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dim == 0) hyper_sweep_lines_kernel<0><<<blocks, threads, 0, s>>>(a);
+  else if (dim == 1) hyper_sweep_lines_kernel<1><<<blocks, threads, 0, s>>>(a);
+  else hyper_sweep_lines_kernel<2><<<blocks, threads, 0, s>>>(a);
+  count_launches(1);
+  return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
+}
+

@@ -88,6 +88,9 @@ class Plan:
         self.h = h
         self.npts = spec.total_points
         self._bufs = {}
+        waves = os.environ.get("HD_SWEEP_WAVES")  # tuning knob, read once per plan
+        if waves:
+            self.set_option(_lib.HD_OPT_SWEEP_WAVES, int(waves))
 
     def __del__(self):
         h = getattr(self, "h", None)

@@ -177,7 +177,7 @@ def test_fast_mode_ke_curve_tracks_exact(hd):
     assert np.all(rel <= 1e-10), rel
 
 
-@pytest.mark.parametrize("n", [(32, 32, 32), (64, 40, 24)])
+@pytest.mark.parametrize("n", [(32, 32, 32), (64, 48, 24)])
 def test_flux_kernel_variants_agree(hd, n):
     """The TMA-fed flux kernel (HD_OPT_FLUX_TMA), the register-prefetch z-marching
     kernel and the pointwise kernel compute the same viscous fluxes (fast mode: the
@@ -204,4 +204,5 @@ def test_flux_kernel_variants_agree(hd, n):
         rel = np.sqrt(((other - outs[0][0]) ** 2).reshape(5, -1).sum(1) /
                       (outs[0][0] ** 2).reshape(5, -1).sum(1))
         assert np.all(rel <= 1e-14), rel
-    assert np.allclose(outs[0][1], outs[1][1], rtol=1e-13) and np.allclose(outs[0][1], outs[2][1], rtol=1e-13)
+    for other in outs[1:]:
+        assert np.allclose(outs[0][1], other[1], rtol=1e-13)
