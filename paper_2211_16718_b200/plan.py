@@ -10,6 +10,7 @@ plan holds ~34 GB, so the cache is small and :func:`release_plans` drops it.
 from __future__ import annotations
 
 import ctypes
+import gc
 import os
 from collections import OrderedDict
 
@@ -332,5 +333,6 @@ def geometry_plan(spec: GridSpec, periodic=(True, True, True)) -> Plan:
 def release_plans() -> None:
     _cache.clear()
     _geo_cache.clear()
+    gc.collect()  # plans referenced only from reference cycles go now, not at the next collection
     if torch.cuda.is_available():
         torch.cuda.empty_cache()

@@ -341,7 +341,9 @@ class _DeviceMarch:
         self.scheme = _SCHEME_CODE[tparams.scheme]
         # multi-rank drivers override how a step runs and how reductions combine
         self.own_stepper = stepper is None and reducer is None
-        self.stepper = stepper or (lambda u, dt_dev, tag: plan.step(self.scheme, u, dt_dev, tag))
+        scheme = self.scheme  # the default stepper must not capture self (a reference cycle
+        # would keep the plan's workspace alive until the next garbage collection)
+        self.stepper = stepper or (lambda u, dt_dev, tag: plan.step(scheme, u, dt_dev, tag))
         self.reducer = reducer or (lambda red: None)
         self.error_combine = error_combine or (lambda key: key)
         # ghosts of the march state valid again after the last step (decomposed runs:
