@@ -516,12 +516,13 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
       const double* w1 = slot(c - 1);
       const double* w2 = slot(c);
       const double* w3 = slot(c + 1);
-      const double* w4 = slot(c + 2);
+      // position c+2 was ingested this iteration: its values are still in registers
 #pragma unroll
       for (int v = 0; v < 2 * NV - 1; ++v) {
         double l, r;
+        const double q4 = v < NV ? wu[4][v] : wf[4][v - NV + 1];
         recon_pair<EXACT>(w0[v * SWEEP_THREADS], w1[v * SWEEP_THREADS], w2[v * SWEEP_THREADS],
-                          w3[v * SWEEP_THREADS], w4[v * SWEEP_THREADS], eps, power, l, r);
+                          w3[v * SWEEP_THREADS], q4, eps, power, l, r);
         if (v < NV) { nu[v] = l; ru[v] = r; }
         else { nf[v - NV + 1] = l; rf[v - NV + 1] = r; }
       }

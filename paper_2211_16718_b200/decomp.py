@@ -488,13 +488,22 @@ class DistHalo:
                 wait(_lib.HD_PEER_STATE, counter[0])
                 plan.fill_ghosts(u, NVARS)
 
+            def protocol_check():
+                # a wait that timed out on any rank ends the march on every rank, at the
+                # next check (every step when the march synchronises, else at its end)
+                flag = torch.tensor([1 if plan.peer_timed_out() else 0], dtype=torch.int64,
+                                    device=state.device)
+                dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
+                _check_protocol(not bool(flag.item()), "a neighbour never signalled (peer halo timed out)")
+
             nblocks = self.layout.dims[0] * self.layout.dims[1] * self.layout.dims[2]
             march = _DeviceMarch(plan, local, gas, tparams, t0, stepper=stepper, reducer=reducer,
                                  global_points=spec.interior_points * nblocks,
                                  copy=False,
                                  error_combine=lambda key: _combine_error_key(key, self.group),
                                  ghost_sync=ghost_sync,
-                                 sum_combine=lambda t: _combine_sums(t, self.group))
+                                 sum_combine=lambda t: _combine_sums(t, self.group),
+                                 protocol_check=protocol_check)
             try:
                 res = march.run(observer, dt_provider)
             finally:

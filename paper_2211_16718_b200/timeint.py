@@ -324,7 +324,7 @@ class _DeviceMarch:
 
     def __init__(self, plan, fields: FieldSet, gas: GasModel, tparams: TimeParams, t0: float,
                  stepper=None, reducer=None, global_points: int | None = None, copy: bool = True,
-                 error_combine=None, ghost_sync=None, sum_combine=None):
+                 error_combine=None, ghost_sync=None, sum_combine=None, protocol_check=None):
         self.plan = plan
         self.spec = fields.spec
         # interior points of the whole (possibly decomposed) domain: the KE mean
@@ -350,6 +350,8 @@ class _DeviceMarch:
         # the final halo), and the rank sum of per-rank partial sums
         self.ghost_sync = ghost_sync or (lambda u: None)
         self.sum_combine = sum_combine or (lambda t: None)
+        # decomposed runs: raise a halo failure (peer timeout) before the error keys it caused
+        self.protocol_check = protocol_check or (lambda: None)
 
     def _enstrophy_now(self, dst: torch.Tensor) -> None:
         """Enstrophy sum of the current state into ``dst`` (one element)."""
@@ -526,6 +528,7 @@ class _DeviceMarch:
     def _check(self, step_base: int) -> None:
         """Raise the latched error; multi-rank drivers combine the keys first
         (``error_combine``) so every rank raises the same error at the same step."""
+        self.protocol_check()
         key = self.error_combine(self.plan.error_key())
         if key:
             self.plan.error_clear()
