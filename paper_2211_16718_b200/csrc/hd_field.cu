@@ -703,12 +703,14 @@ static bool launch_flux_tma_cfg(const hd_plan* p, const double* u, dim3 grid, di
                                 double* partial, cudaStream_t s) {
   CUtensorMap tm;
   if (!state_tensor_map(p, u, C::PY, &tm)) return false;
-  static bool attr = false;
-  if (!attr) {
+  // the dynamic shared-memory opt-in is per device context: once per device
+  static bool attr[64] = {};
+  const int dev = p->device >= 0 && p->device < 64 ? p->device : 0;
+  if (!attr[dev]) {
     if (cudaFuncSetAttribute(gradflux_tma_kernel<ENS, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sizeof(typename C::Smem)) != cudaSuccess)
       return false;
-    attr = true;
+    attr[dev] = true;
   }
   const double mu = p->phys.mu;
   const double q_coef = (-mu) / ((p->phys.gamma - 1.0) * p->phys.prandtl);  // viscous.py:107
