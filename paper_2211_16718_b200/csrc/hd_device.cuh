@@ -289,6 +289,33 @@ __device__ __forceinline__ void rk_store_pre(const RKArgs& r, const Geo& G, int 
   store_point_images<NV>(dst, G.npts, q, nd, dl, outv);
 }
 
+// rk_store_pre for the classical RK4 tableau with the stage kind fixed at compile
+// time: K = 0 stage 0 (acc = k), 1 stages 1-2 (acc += 2k), 2 stage 3 (u + dt/6 (acc + k)).
+// The same roundings as the generic path: out = u0 + (kad acc + round(kcd k)).
+template <int K>  // 0, 1, 2 only
+__device__ __forceinline__ void rk4_store(const RKArgs& r, const Geo& G, int i, int j, int k,
+                                          const double (&kv)[NV], const double (&u0)[NV],
+                                          const double (&acc)[NV], double (&outv)[NV]) {
+  static_assert(K >= 0 && K <= 2, "RK4 stage kind");
+  const double dt = *r.dt;
+  const int64_t q = G.idx(i, j, k);
+  const double kcd = r.kc * dt;
+  double* dst = K == 2 ? r.u : r.stage_out;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const double kk = __dmul_rn(kcd, kv[v]);
+    if constexpr (K == 2) {
+      outv[v] = __dadd_rn(u0[v], fma(r.ka * dt, acc[v], kk));
+    } else {
+      outv[v] = __dadd_rn(u0[v], kk);
+      r.acc[q + v * G.npts] = K == 0 ? kv[v] : fma(1.0, acc[v], 2.0 * kv[v]);
+    }
+  }
+  int64_t dl[6];
+  const int nd = face_image_deltas(G, i, j, k, periodic_mask(G), dl);
+  store_point_images<NV>(dst, G.npts, q, nd, dl, outv);
+}
+
 RKArgs make_rk(const hd_plan* p, int scheme, int stage, double* u, const double* dt_dev);
 
 // kv[row] += D_d F_d[row-1] for the dims in dmask, in the order d = 0, 1, 2 and

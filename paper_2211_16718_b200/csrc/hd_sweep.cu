@@ -318,7 +318,13 @@ template <int DIM> struct SweepCfg {
 // ROLE_UPDATE_DIAG: ROLE_UPDATE of the last stage with the diagnostics of the new
 // state folded in (hd_arm_reduce) -- a separate instantiation, so the other stages'
 // update kernel carries none of its registers
+// ROLE_RK4_*: ROLE_UPDATE specialised to the stages of the classical RK4 tableau
+// (timeint.py:181-193), so no run-time flag, predicated load or unused operand
+// remains: A = stage 0 (acc = k, no accumulator read), B = stages 1, 2 (acc += 2k),
+// C = stage 3 (u + dt/6 (acc + k), no accumulator write), C_DIAG = C with the
+// diagnostics.  ROLE_UPDATE / ROLE_UPDATE_DIAG stay the generic (TVD-RK3) path.
 constexpr int ROLE_PLAIN = 0, ROLE_VISC = 1, ROLE_UPDATE = 2, ROLE_UPDATE_DIAG = 3;
+constexpr int ROLE_RK4_A = 4, ROLE_RK4_B = 5, ROLE_RK4_C = 6, ROLE_RK4_C_DIAG = 7;
 
 struct SweepArgs {
   Geo geo;
@@ -400,8 +406,10 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
   // the previous iteration and the store into the ring stalled on them (ncu: 20%
   // of the y sweep's and 24% of the z sweep's warp samples).
   constexpr bool VROLE = ROLE != ROLE_PLAIN;
-  constexpr bool UPD = ROLE == ROLE_UPDATE || ROLE == ROLE_UPDATE_DIAG;
-  constexpr bool DIAG = ROLE == ROLE_UPDATE_DIAG && !EXACT;
+  constexpr bool UPD = ROLE >= ROLE_UPDATE;
+  constexpr bool DIAG = (ROLE == ROLE_UPDATE_DIAG || ROLE == ROLE_RK4_C_DIAG) && !EXACT;
+  constexpr bool RK4S = ROLE >= ROLE_RK4_A;  // a specialised RK4 stage
+  constexpr bool READ_ACC = ROLE == ROLE_RK4_B || ROLE == ROLE_RK4_C || ROLE == ROLE_RK4_C_DIAG;
   constexpr bool FWIN = VROLE && SMEM_WINDOW;
   constexpr int FS = 6;  // flux ring slots: positions c-3 .. c+2 at iteration c
   __shared__ double ring[SMEM_WINDOW ? 5 * 9 * SWEEP_THREADS : 1];
@@ -503,7 +511,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         ru0[v] = wr ? a.rk.u[qo + v * np] : 0.0;
-        racc[v] = (wr && a.rk.rd_acc) ? a.rk.acc[qo + v * np] : 0.0;
+        if constexpr (RK4S) racc[v] = (READ_ACC && wr) ? a.rk.acc[qo + v * np] : 0.0;
+        else racc[v] = (wr && a.rk.rd_acc) ? a.rk.acc[qo + v * np] : 0.0;
       }
     }
     double old[NV];
@@ -573,7 +582,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
           else if (DIM == 1) cj = c - 1;
           else ck = c - 1;
           double out[NV];
-          rk_store_pre(a.rk, G, ci, cj, ck, val, ru0, racc, out);
+          if constexpr (RK4S)
+            rk4_store<ROLE == ROLE_RK4_A ? 0 : (ROLE == ROLE_RK4_B ? 1 : 2)>(a.rk, G, ci, cj, ck, val, ru0, racc, out);
+          else rk_store_pre(a.rk, G, ci, cj, ck, val, ru0, racc, out);
           if constexpr (DIAG) {
             const int code = diag_fast(out, a.ph.gamma, a.rh[0], a.rh[1], a.rh[2], diag);
             if (code) latch_error(a.err, a.fred_tag, code, G.idx(ci, cj, ck));
@@ -870,15 +881,22 @@ int launch_sweep_update(const hd_plan* p, const double* u_stage, double* inc, co
   const Geo& G = p->geo;
   const int64_t warps = (int64_t)(G.n[0] / 32) * G.n[1] * nseg;
   if (fused) *fused = 0;
+  const bool rk4 = scheme == HD_SCHEME_RK4;
   if (red_out && a.rk.to_u && G.n[0] % 32 == 0 && G.n[1] % 2 == 0 &&
       warps <= fused_red_capacity(p->geom)) {
     a.fred = (double*)(p->ws + p->off[HD_BUF_FRED]);
     a.fred_tag = red_tag;
     for (int d = 0; d < 3; ++d) a.rh[d] = 1.0 / G.h[d];
-    int rc = launch_dim<2, false, ROLE_UPDATE_DIAG>(p, a, nseg, s);
+    int rc = rk4 ? launch_dim<2, false, ROLE_RK4_C_DIAG>(p, a, nseg, s)
+                 : launch_dim<2, false, ROLE_UPDATE_DIAG>(p, a, nseg, s);
     if (!rc) rc = launch_reduce_finish(a.fred, (int)warps, red_out, s);
     if (!rc && fused) *fused = 1;
     return rc;
+  }
+  if (rk4) {
+    if (stage == 0) return launch_dim<2, false, ROLE_RK4_A>(p, a, nseg, s);
+    if (stage < 3) return launch_dim<2, false, ROLE_RK4_B>(p, a, nseg, s);
+    return launch_dim<2, false, ROLE_RK4_C>(p, a, nseg, s);
   }
   return launch_dim<2, false, ROLE_UPDATE>(p, a, nseg, s);
 }
