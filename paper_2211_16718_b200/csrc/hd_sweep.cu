@@ -645,12 +645,19 @@ constexpr int XS_PAD = XC + 1;
 // dynamic shared memory per block, same 4 blocks/SM) measured slower: 8.5 -> 10.3
 // ms at 512^3
 constexpr int XB = 2;
+// Output ring of XO = 8 cells per row (pitch XO + 1, odd): a flush writes each
+// row's increments in groups that start on a 32-byte sector boundary of that row
+// (rows of n_x + 2g doubles alternate between two sector phases), so every
+// group is one full sector instead of two partial ones -- ncu at 512^3: L2 write
+// sectors 335.5M -> see DESIGN.md section 8.
+constexpr int XO = 8;
+constexpr int XO_PAD = XO + 1;
 
 template <bool EXACT, int PW>
 __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_staged_kernel(const SweepArgs a) {
   constexpr int WARPS = SWEEP_THREADS / 32;
   __shared__ double xin[WARPS][XB][NV][32 * XS_PAD];
-  __shared__ double xout[WARPS][NV][32 * XS_PAD];
+  __shared__ double xout[WARPS][NV][32 * XO_PAD];
   const Geo& G = a.geo;
   const int lane = threadIdx.x, w = threadIdx.y;
   const int j0 = blockIdx.x * 32;  // launch guarantees n_y % 32 == 0
@@ -698,19 +705,26 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
       if (code) latch_error(a.err, a.tag, code, first_image(G, p, j0 + lane, k));
     }
   };
-  // out chunk: cells c0 + XC t .. ; d[v] staged, flushed coalesced as inc = old - d
+  // out: cell c0 + i staged in ring slot i % XO; flush t writes, per row, the
+  // XC = 4 cells [L, L + 4) with L = 4t + e - (e ? 4 : 0), e = cells before the
+  // row's first sector boundary -- after flush t every cell < 4t + e of the row
+  // is written, the ring holds cells 4t-3 .. 4t+3 while a flush reads them.
+  // inc = old - d, coalesced: 4 lanes fill one sector of one row.
+  const int seg_len = c1 - c0;
   auto flush = [&](int t) {
     __syncwarp();
     const int xo = lane % XC;
-    const int m = c0 + XC * t + xo;
-    if (m < c1) {
 #pragma unroll
-      for (int i = 0; i < XC; ++i) {
-        const int r = RPI * i + lane / XC;
-        double* dst = a.inc + row0 + (int64_t)r * sy + m;
+    for (int i = 0; i < XC; ++i) {
+      const int r = RPI * i + lane / XC;
+      double* row = a.inc + row0 + (int64_t)r * sy + c0;
+      const int e = (int)((0u - (unsigned)((uintptr_t)row >> 3)) & 3u);
+      const int cell = XC * t + e - (e ? XC : 0) + xo;
+      if (cell >= 0 && cell < seg_len) {
+        double* dst = row + cell;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          const double d = xout[w][v][r * XS_PAD + xo];
+          const double d = xout[w][v][r * XO_PAD + (cell % XO)];
           const double old = a.accumulate ? dst[v * np] : 0.0;
           if constexpr (EXACT) dst[v * np] = xs(old, d);
           else dst[v * np] = old - d;
@@ -766,16 +780,19 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
       double flux[NV];
       roe_flux<0, EXACT>(lu, ru, lf, rf, a.ph, flux);
       if (c > c0) {
-        const int m = c - 1;
-        const int oo = (m - c0) % XC;
+        const int i = c - 1 - c0;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           double d;
           if constexpr (EXACT) d = xm(xs(flux[v], fprev[v]), a.inv_dx);
           else d = (flux[v] - fprev[v]) * a.inv_dx;
-          xout[w][v][lane * XS_PAD + oo] = d;
+          xout[w][v][lane * XO_PAD + (i % XO)] = d;
         }
-        if (oo == XC - 1 || m == c1 - 1) flush((m - c0) / XC);
+        if (i % XC == XC - 1) flush(i / XC);
+        if (i == seg_len - 1) {
+          if (i % XC != XC - 1) flush(i / XC);
+          flush(i / XC + 1);
+        }
       }
 #pragma unroll
       for (int v = 0; v < NV; ++v) fprev[v] = flux[v];
