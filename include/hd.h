@@ -62,7 +62,7 @@ extern "C" {
 #define HD_OPT_X_STAGED 1      /* 1 (default): cp.async-staged x sweep when n_y % 32 == 0; 0: plain */
 #define HD_OPT_FLUX_ZMARCH 2   /* 1 (default): z-marching viscous flux kernel when the tiles fit; 0: pointwise */
 #define HD_OPT_FLUX_TMA 3      /* 1 (default): fast-mode flux kernel fed by TMA when the state maps to a tensor */
-#define HD_OPT_SWEEP_WAVES 4   /* automatic sweep segments: lines x segments >= this many waves of 256 threads/SM (default 6) */
+#define HD_OPT_SWEEP_WAVES 4   /* automatic sweep segments: 0 (default) = wave-quantisation model; k > 0 = lines x segments >= k waves of 256 threads/SM */
 #define HD_OPT_N 5
 
 /* workspace buffers (hd_plan_buffer) */

@@ -164,7 +164,7 @@ int hd_plan_create(const hd_geom* geom, const hd_gas* gas, const hd_weno* weno, 
   p->opt[HD_OPT_X_STAGED] = 1;
   p->opt[HD_OPT_FLUX_ZMARCH] = 1;
   p->opt[HD_OPT_FLUX_TMA] = 1;
-  p->opt[HD_OPT_SWEEP_WAVES] = 6;
+  p->opt[HD_OPT_SWEEP_WAVES] = 0;  // 0: the wave-quantisation model (hd_sweep.cu)
   std::memcpy(p->off, off, sizeof(off));
   if (cudaGetDevice(&p->device) != cudaSuccess ||
       cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device) != cudaSuccess) {

@@ -822,6 +822,56 @@ static int launch_dim(const hd_plan* p, const SweepArgs& a, int nseg, cudaStream
   return cudaGetLastError() == cudaSuccess ? HD_OK : HD_E_CUDA;
 }
 
+// Resident warps per SM of the fast-mode kernel each axis launches in a step
+// (staged x sweep, y VISC, z RK4 stage), queried once per process.
+static int sweep_warps_per_sm(int dim) {
+  static int cached[3] = {0, 0, 0};
+  if (cached[dim] > 0) return cached[dim];
+  int blocks = 0;
+  cudaError_t e;
+  if (dim == 0) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, sweep_x_staged_kernel<false, 2>, SWEEP_THREADS, 0);
+  else if (dim == 1) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, sweep_kernel<1, false, ROLE_VISC, 2>, SWEEP_THREADS, 0);
+  else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, sweep_kernel<2, false, ROLE_RK4_B, 2>, SWEEP_THREADS, 0);
+  if (e != cudaSuccess || blocks < 1) {
+    (void)cudaGetLastError();
+    return SWEEP_THREADS / 32 * SweepCfg<0>::min_blocks;  // not cached: retry next launch
+  }
+  return cached[dim] = blocks * (SWEEP_THREADS / 32);
+}
+
+// Segments per line.  A segment of L cells costs about L + SEG_RESTART cells of
+// work (the window refill and the extra interface flux at its start), and a
+// launch of W waves of resident warps takes about ceil(W) wave times, since the
+// warps of a sweep march in step and a partial last wave idles the rest of the
+// SMs; pick the count minimising ceil(W) (L + SEG_RESTART) among those giving at
+// least two waves (below that the schedulers lack warps to hide latency: a
+// single 86 %-full wave of the y sweep measured 7 % slower than 2.9 waves of
+// shorter segments).  Measured per axis (tools/gpu/seg_probe.py) it matches the
+// round-1 rule at 512^3 and 256^3 and beats it on small blocks: 128^3 2.61 ->
+// 2.44 ms per step (x sweep -9 %, z sweep -13 %), z -3 % on 256x256x64.
+constexpr int SEG_RESTART = 8;
+constexpr int SEG_MIN_WAVES = 2;
+static int model_segments(int64_t lines, int n, int64_t warp_slots) {
+  int best = 1;
+  double best_cost = 0.0;
+  bool best_full = false;
+  const int max_seg = n / 8 > 0 ? n / 8 : 1;
+  for (int ns = 1; ns <= max_seg; ++ns) {
+    const int len = (n + ns - 1) / ns;
+    if (ns > 1 && (n + len - 1) / len != ns) continue;  // same split as a smaller count
+    const int64_t warps = (lines + 31) / 32 * ns;
+    const int64_t waves = (warps + warp_slots - 1) / warp_slots;
+    const bool full = warps >= SEG_MIN_WAVES * warp_slots;
+    const double cost = (double)waves * (len + SEG_RESTART);
+    if (ns == 1 || (full && !best_full) || (full == best_full && cost < best_cost)) {
+      best = ns;
+      best_cost = cost;
+      best_full = full;
+    }
+  }
+  return best;
+}
+
 static SweepArgs make_args(const hd_plan* p, int dim, const double* u, double* inc, int accumulate,
                            int check, int64_t tag, int& nseg) {
   const Geo& G = p->geo;
@@ -836,13 +886,17 @@ static SweepArgs make_args(const hd_plan* p, int dim, const double* u, double* i
   a.check = check;
   a.err = (unsigned long long*)(p->ws + p->off[HD_BUF_ERR]);
   a.tag = tag;
-  // segment length: enough independent lines to fill ~6 waves of 148 SMs x 256 threads
   const int64_t lines = (int64_t)G.n[0] * G.n[1] * G.n[2] / G.n[dim];
-  const int64_t waves = p->opt[HD_OPT_SWEEP_WAVES] > 0 ? p->opt[HD_OPT_SWEEP_WAVES] : 6;
-  const int64_t target = (int64_t)p->sm_count * 256 * waves;
-  nseg = (int)((target + lines - 1) / lines);
-  if (nseg < 1) nseg = 1;
-  if (nseg > G.n[dim] / 8) nseg = G.n[dim] / 8 > 0 ? G.n[dim] / 8 : 1;
+  if (p->opt[HD_OPT_SWEEP_WAVES] > 0) {
+    // the round-1 rule: enough independent lines to fill this many waves of
+    // 148 SMs x 256 threads
+    const int64_t target = (int64_t)p->sm_count * 256 * p->opt[HD_OPT_SWEEP_WAVES];
+    nseg = (int)((target + lines - 1) / lines);
+    if (nseg < 1) nseg = 1;
+    if (nseg > G.n[dim] / 8) nseg = G.n[dim] / 8 > 0 ? G.n[dim] / 8 : 1;
+  } else {
+    nseg = model_segments(lines, G.n[dim], (int64_t)p->sm_count * sweep_warps_per_sm(dim));
+  }
   // HD_OPT_SEGMENTS (tests: results must not depend on the split)
   if (p->opt[HD_OPT_SEGMENTS] >= 1 && p->opt[HD_OPT_SEGMENTS] <= G.n[dim]) nseg = (int)p->opt[HD_OPT_SEGMENTS];
   a.seg = (G.n[dim] + nseg - 1) / nseg;
