@@ -78,13 +78,17 @@ __device__ __forceinline__ void recon_pair(double q0, double q1, double q2, doub
     //   D0-4D1 (right).
     const double D0 = q1 - q0, D1 = q2 - q1, D2 = q3 - q2, D3 = q4 - q3;
     // expanded: 12 beta1 = 13 t1^2 + 3 s1^2 = 4 (10 D1^2 - 11 D0 D1 + 4 D0^2), and
-    // likewise 3 beta2 = 4 D1^2 - 5 D1 D2 + 4 D2^2, 3 beta3 = 10 D2^2 - 11 D2 D3 + 4 D3^2
-    // (weights scaled by a common factor 3, eps with them)
-    const double S0 = D0 * D0, S1 = D1 * D1, S2 = D2 * D2, S3 = D3 * D3;
-    const double eps3 = 3.0 * eps;
-    const double d1 = fma(10.0, S1, fma(-11.0 * D0, D1, fma(4.0, S0, eps3)));
-    const double d2 = fma(4.0, S1 + S2, fma(-5.0 * D1, D2, eps3));
-    const double d3 = fma(10.0, S2, fma(-11.0 * D2, D3, fma(4.0, S3, eps3)));
+    // likewise 3 beta2 = 4 D1^2 - 5 D1 D2 + 4 D2^2, 3 beta3 = 10 D2^2 - 11 D2 D3 + 4 D3^2;
+    // all three (and eps) scaled by the common factor 3/4, which cancels in the
+    // normalised weights, and factored so every constant is exact and each
+    // indicator is two FMAs on a shared square:
+    //   d1 = D0 (D0 - 2.75 D1) + 2.5 D1^2,  d2 = D1 (D1 - 1.25 D2) + D2^2,
+    //   d3 = D3 (D3 - 2.75 D2) + 2.5 D2^2   (11 FP64 operations instead of 16)
+    const double S1 = D1 * D1, S2 = D2 * D2;
+    const double epsq = 0.75 * eps;
+    const double d1 = fma(D0, fma(-2.75, D1, D0), fma(2.5, S1, epsq));
+    const double d2 = fma(D1, fma(-1.25, D2, D1), S2 + epsq);
+    const double d3 = fma(D3, fma(-2.75, D2, D3), fma(2.5, S2, epsq));
     double e1 = d1, e2 = d2, e3 = d3;
     for (int q = 0; q < power - 1; ++q) {
       e1 *= d1;
