@@ -96,15 +96,21 @@ __device__ __forceinline__ void recon_pair(double q0, double q1, double q2, doub
       e3 *= d3;
     }
     const double e12 = e1 * e2, e13 = e1 * e3, e23 = e2 * e3;
-    const double mid = 6.0 * e13;  // 0.6/e2 weight, both sides (x10 scaling cancels)
-    // left: (0.1/e1, 0.6/e2, 0.3/e3) ~ (e23, 6 e13, 3 e12)
-    const double nl1 = e23, nl3 = 3.0 * e12;
-    const double al1 = fma(5.0, D1, -2.0 * D0), al2 = fma(2.0, D2, D1), al3 = fma(4.0, D2, -D3);
-    left = fma(fma(nl1, al1, fma(mid, al2, nl3 * al3)), frcp_weights(6.0 * ((nl1 + mid) + nl3)), q2);
-    // right (mirrored): (0.1/e3, 0.6/e2, 0.3/e1) ~ (e12, 6 e13, 3 e23)
-    const double nr1 = e12, nr3 = 3.0 * e23;
-    const double ar1 = fma(-5.0, D2, 2.0 * D3), ar2 = fma(2.0, D1, D2), ar3 = fma(-4.0, D1, D0);
-    right = fma(fma(nr1, ar1, fma(-mid, ar2, nr3 * ar3)), frcp_weights(6.0 * ((nr1 + mid) + nr3)), q2);
+    // left: weights (0.1/e1, 0.6/e2, 0.3/e3) ~ (e23, 6 e13, 3 e12), corrections
+    // (c_k - q2) = (5D1-2D0)/6, (D1+2D2)/6, (4D2-D3)/6; the 1/6 goes into the
+    // numerator's weights (6 e13 / 6 = e13, 3 e12 / 6 = e12 / 2) except for the
+    // first term, whose correction takes it (5/6 D1 - 1/3 D0), so the normaliser
+    // is two FMAs on the products: 13 operations per side instead of 14.5
+    const double al1 = fma(5.0 / 6.0, D1, (-1.0 / 3.0) * D0), al2 = fma(2.0, D2, D1),
+                 al3 = fma(4.0, D2, -D3);
+    const double numl = fma(e23, al1, fma(e13, al2, (0.5 * e12) * al3));
+    left = fma(numl, frcp_weights(fma(6.0, e13, fma(3.0, e12, e23))), q2);
+    // right (mirrored): (0.1/e3, 0.6/e2, 0.3/e1) ~ (e12, 6 e13, 3 e23), corrections
+    // (2D3-5D2)/6, -(D2+2D1)/6, (D0-4D1)/6
+    const double ar1 = fma(-5.0 / 6.0, D2, (1.0 / 3.0) * D3), ar2 = fma(2.0, D1, D2),
+                 ar3 = fma(-4.0, D1, D0);
+    const double numr = fma(e12, ar1, fma(-e13, ar2, (0.5 * e23) * ar3));
+    right = fma(numr, frcp_weights(fma(6.0, e13, fma(3.0, e23, e12))), q2);
   }
 }
 
