@@ -47,7 +47,10 @@ __device__ __forceinline__ double frcp(double x) {
 
 // Reciprocal for the WENO weight normalisation: one Newton step.  It only
 // scales the correction term sum_k w_k (c_k - q2) (recon_pair), so its relative
-// error (~1e-14) enters the reconstructed value scaled by |c_k - q2| / |q2|.
+// error enters the reconstructed value scaled by |c_k - q2| / |q2|.  Measured on
+// B200 (tools/gpu/approx_acc.cu, log-uniform inputs): the MUFU seed is good to
+// 9.9e-7, one Newton step to 9.9e-13, two to the IEEE result -- which is why the
+// flux inputs (frcp) take two.
 __device__ __forceinline__ double frcp_weights(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
