@@ -62,6 +62,9 @@ __device__ __forceinline__ double recon5_exact(double f0, double f1, double f2, 
 // (weno.py:9-11), so beta/eps terms are computed once; the three normalised
 // weights of each side share one reciprocal:
 //   w_k = (g_k / e_k) / sum_j (g_j / e_j) = g_k prod_{j!=k} e_j / sum_j g_j prod_{i!=j} e_i.
+__device__ __forceinline__ void recon_pair_d(double D0, double D1, double D2, double D3, double q2,
+                                             double eps, int power, double& left, double& right);
+
 template <bool EXACT>
 __device__ __forceinline__ void recon_pair(double q0, double q1, double q2, double q3, double q4,
                                            double eps, int power, double& left, double& right) {
@@ -69,6 +72,15 @@ __device__ __forceinline__ void recon_pair(double q0, double q1, double q2, doub
     left = recon5_exact(q0, q1, q2, q3, q4, eps, power);
     right = recon5_exact(q4, q3, q2, q1, q0, eps, power);
   } else {
+    recon_pair_d(q1 - q0, q2 - q1, q3 - q2, q4 - q3, q2, eps, power, left, right);
+  }
+}
+
+// The fast pair from the window's first differences D_i = q_{i+1} - q_i and its
+// centre q2 (a marching window can carry the differences instead of the values).
+__device__ __forceinline__ void recon_pair_d(double D0, double D1, double D2, double D3, double q2,
+                                             double eps, int power, double& left, double& right) {
+  {
     // Everything in first differences D_i = q_{i+1} - q_i of the window:
     //   beta_k = 13/12 t_k^2 + 1/4 s_k^2 with t1 = D1-D0, s1 = 3D1-D0, t2 = D2-D1,
     //   s2 = -(D1+D2), t3 = D3-D2, s3 = D3-3D2 (scaled by 12; the common factor
@@ -76,7 +88,6 @@ __device__ __forceinline__ void recon_pair(double q0, double q1, double q2, doub
     //   weights sum to one each value is q2 + sum_k w_k (c_k - q2), with
     //   6 (c_k - q2) = 5D1-2D0, D1+2D2, 4D2-D3 (left) and 2D3-5D2, -(D2+2D1),
     //   D0-4D1 (right).
-    const double D0 = q1 - q0, D1 = q2 - q1, D2 = q3 - q2, D3 = q4 - q3;
     // expanded: 12 beta1 = 13 t1^2 + 3 s1^2 = 4 (10 D1^2 - 11 D0 D1 + 4 D0^2), and
     // likewise 3 beta2 = 4 D1^2 - 5 D1 D2 + 4 D2^2, 3 beta3 = 10 D2^2 - 11 D2 D3 + 4 D3^2;
     // all three (and eps) scaled by the common factor 3/4, which cancels in the
@@ -744,7 +755,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
     __syncwarp();
   };
 
-  double wu[5][NV], wf[5][NV];
+  // Register window.  Exact: the five positions c-2 .. c+2 (wu/wf[0..4]).  Fast:
+  // the differences D0..D2 of positions c-2 .. c+1 and the value at c+1 -- four
+  // values per variable instead of five; each position difference is formed once
+  // (not four times), and the centre is q2 = q(c+1) - D2: 2 instead of 4 FP64
+  // operations per reconstruction pair and 18 fewer registers.
+  double wu[EXACT ? 5 : 4][NV], wf[EXACT ? 5 : 4][NV];
   // Entering chunk t (its first position is consumed): wait for it -- it was
   // issued when chunk t-XB+1 was entered, later chunks may still be in flight --
   // then issue chunk t+XB-1 into the buffer chunk t-1 has vacated.  Positions
@@ -758,7 +774,22 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
       __syncwarp();
       issue(q / XC + XB - 1);
     }
-    take(p0 + q, wu[q + 1], wf[q + 1]);
+    if constexpr (EXACT) {
+      take(p0 + q, wu[q + 1], wf[q + 1]);
+    } else {
+      // wu[3] holds the newest value; wu[q-1] = its difference to the previous one
+      double nu_[NV], nf_[NV];
+      take(p0 + q, nu_, nf_);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        if (q > 0) {  // never contracted with the flux products: segment-split invariant
+          wu[q - 1][v] = __dsub_rn(nu_[v], wu[3][v]);
+          wf[q - 1][v] = __dsub_rn(nf_[v], wf[3][v]);
+        }
+        wu[3][v] = nu_[v];
+        wf[3][v] = nf_[v];
+      }
+    }
   }
 
   double lu[NV], lf[NV], fprev[NV];
@@ -769,21 +800,46 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SWEEP_MIN_BLOCKS_X) sweep_x_sta
       __syncwarp();
       issue((p - p0) / XC + XB - 1);
     }
+    double ru[NV], rf[NV], nu[NV], nf[NV];
+    if constexpr (EXACT) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          wu[q][v] = wu[q + 1][v];
+          wf[q][v] = wf[q + 1][v];
+        }
+      take(p, wu[4], wf[4]);
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+        recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
+#pragma unroll
+      for (int v = 1; v < NV; ++v)
+        recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
+    } else {
+      double qu[NV], qf[NV];
+      take(p, qu, qf);
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        wu[q][v] = wu[q + 1][v];
-        wf[q][v] = wf[q + 1][v];
+        const double D3 = __dsub_rn(qu[v], wu[3][v]);
+        recon_pair_d(wu[0][v], wu[1][v], wu[2][v], D3, __dsub_rn(wu[3][v], wu[2][v]), eps, power, nu[v],
+                     ru[v]);
+        wu[0][v] = wu[1][v];
+        wu[1][v] = wu[2][v];
+        wu[2][v] = D3;
+        wu[3][v] = qu[v];
       }
-    take(p, wu[4], wf[4]);
-    double ru[NV], rf[NV], nu[NV], nf[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
-      recon_pair<EXACT>(wu[0][v], wu[1][v], wu[2][v], wu[3][v], wu[4][v], eps, power, nu[v], ru[v]);
-#pragma unroll
-    for (int v = 1; v < NV; ++v)
-      recon_pair<EXACT>(wf[0][v], wf[1][v], wf[2][v], wf[3][v], wf[4][v], eps, power, nf[v], rf[v]);
+      for (int v = 1; v < NV; ++v) {
+        const double D3 = __dsub_rn(qf[v], wf[3][v]);
+        recon_pair_d(wf[0][v], wf[1][v], wf[2][v], D3, __dsub_rn(wf[3][v], wf[2][v]), eps, power, nf[v],
+                     rf[v]);
+        wf[0][v] = wf[1][v];
+        wf[1][v] = wf[2][v];
+        wf[2][v] = D3;
+        wf[3][v] = qf[v];
+      }
+    }
     nf[0] = nu[1];
     rf[0] = ru[1];
     if (c >= c0) {
