@@ -159,7 +159,8 @@ class Plan:
 
     def set_option(self, option: int, value: int) -> None:
         """Kernel selection (HD_OPT_*): sweep segments per line, staged x sweep,
-        z-marching flux kernel.  Results never depend on it."""
+        z-marching flux kernel.  The state and dt never depend on it (the fused
+        diagnostics' summation order follows the z sweep's segmentation)."""
         _lib.check(self.L.hd_plan_set_option(self.h, option, int(value)), "hd_plan_set_option")
 
     def stage_part(self, scheme: int, stage: int, parts: int, u, dt_dev, tag: int) -> None:
