@@ -652,9 +652,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, SweepCfg<DIM>::min_blocks) swee
 // plain kernel's per-lane loads and stores touch 32 different rows (one sector
 // per lane: partial-sector writes, L1 thrash).  Here the warp moves 4-point
 // chunks of all 32 rows with cp.async (lane l copies row 8i + l/4, position
-// l%4: four full 32-byte sectors per instruction), in a ring of XB buffers
-// filled XB-1 chunks ahead, and its increments go out the same way through a
-// staging tile.
+// l%4: 32 contiguous bytes of each of 8 rows per instruction), in a ring of XB
+// buffers filled XB-1 chunks ahead, and its increments go out through an 8-cell
+// ring in groups aligned to each row's 32-byte sectors (XO below).
 // ---------------------------------------------------------------------------
 // Chunks of XC = 4 positions per row; staging tiles have row pitch XC + 1
 // doubles (odd: conflict-free 64-bit access).  Chunks of 2 with a shared-memory
