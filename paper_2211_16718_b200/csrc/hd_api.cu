@@ -171,6 +171,7 @@ int hd_plan_create(const hd_geom* geom, const hd_gas* gas, const hd_weno* weno, 
     delete p;
     return HD_E_CUDA;
   }
+  sweep_occupancy_warm();
   // error key starts at "none"; context zeroed
   if (p->ws && (cudaMemset(p->ws + p->off[HD_BUF_ERR], 0xff, 8) != cudaSuccess ||
       cudaMemset(p->ws + p->off[HD_BUF_CTX], 0, 8 * HD_CTX_N) != cudaSuccess)) {

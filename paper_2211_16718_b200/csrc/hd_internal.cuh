@@ -133,6 +133,9 @@ namespace hd {
 // number of kernels this library has launched (hd_launch_counter)
 void count_launches(int n);
 // launchers implemented in the .cu files
+// occupancy queries behind the sweep segment model, done once per process at plan
+// creation (never first inside a stream capture)
+void sweep_occupancy_warm();
 int launch_sweep(const hd_plan* p, int dim, const double* u, double* inc, int accumulate,
                  int check, int64_t tag, cudaStream_t s);
 // fused stage pipeline (fast mode): y sweep + x/y viscous divergence; z sweep +

@@ -905,6 +905,10 @@ static int sweep_warps_per_sm(int dim) {
   return cached[dim] = blocks * (SWEEP_THREADS / 32);
 }
 
+void sweep_occupancy_warm() {
+  for (int d = 0; d < 3; ++d) (void)sweep_warps_per_sm(d);
+}
+
 // Segments per line.  A segment of L cells costs about L + SEG_RESTART cells of
 // work (the window refill and the extra interface flux at its start), and a
 // launch of W waves of resident warps takes about ceil(W) wave times, since the
