@@ -917,8 +917,8 @@ void sweep_occupancy_warm() {
 // least two waves (below that the schedulers lack warps to hide latency: a
 // single 86 %-full wave of the y sweep measured 7 % slower than 2.9 waves of
 // shorter segments).  Measured per axis (tools/gpu/seg_probe.py) it matches the
-// round-1 rule at 512^3 and 256^3 and beats it on small blocks: 128^3 2.61 ->
-// 2.44 ms per step (x sweep -9 %, z sweep -13 %), z -3 % on 256x256x64.
+// round-1 rule at 512^3 and 256^3 and beats it on small blocks: 128^3 2.59 ->
+// 2.46 ms per step (x sweep -4 %, y -4 %, z sweep -9 %), -3 % on 256x256x64.
 constexpr int SEG_RESTART = 8;
 constexpr int SEG_MIN_WAVES = 2;
 static int model_segments(int64_t lines, int n, int64_t warp_slots) {
